@@ -1,0 +1,204 @@
+/*
+ * ssb.h — C ABI of the B200 batched serving-scheduler simulator (libssb.so).
+ *
+ * This is the drop-in boundary for the reference's simulation path
+ * (servesim, /root/reference/pkg/src/servesim). One call simulates a batch of
+ * independent *instances*; an instance is exactly one reference
+ * `run_cluster(settings, trace)` call (cluster.py:65-174), and with
+ * n_servers == 1 it is also exactly one `Engine(...).run(trace)` call
+ * (engine.py:236-265, equivalence pinned by tests/test_cluster.py:39-60).
+ *
+ * Plugin surface mirrored:
+ *   - scheduler registry  POLICY_NAMES   policies.py:279 / make_policy   policies.py:282
+ *   - balancer registry   BALANCER_NAMES balancers.py:219 / make_balancer balancers.py:222
+ *   - EngineSettings / BalancerSettings / ClusterSettings fields   config.py:26-56
+ * Custom Python SchedulerPolicy/LoadBalancer subclasses have no ABI: the host
+ * shim rejects them (there is no CPU fallback).
+ *
+ * Conventions: every pointer handed to ssb_simulate/ssb_summarize is a DEVICE
+ * pointer owned by the caller; the library never allocates device memory on
+ * its own. Calls are asynchronous on the given stream. All times are
+ * IEEE-754 binary64 seconds; all token counts are exact integers.
+ */
+#ifndef SSB_H_
+#define SSB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSB_ABI_VERSION 1
+
+/* scheduler registry keys, policies.py:279 ("fcfs","nopreempt","trail_plus","larry") */
+enum { SSB_POLICY_FCFS = 0, SSB_POLICY_NOPREEMPT = 1, SSB_POLICY_TRAIL_PLUS = 2, SSB_POLICY_LARRY = 3 };
+/* balancer registry keys, balancers.py:219 ("rr","random","p2c","sal") */
+enum { SSB_BAL_RR = 0, SSB_BAL_RANDOM = 1, SSB_BAL_P2C = 2, SSB_BAL_SAL = 3 };
+
+/* status codes (per instance and per call) */
+enum {
+  SSB_OK = 0,
+  SSB_E_INFEASIBLE = 1,  /* policies.py:56-68,119-131 InfeasibleRequestError (host pre-checks) */
+  SSB_E_STALL = 2,       /* engine.py:209-214 StallError                                      */
+  SSB_E_CAPACITY = 3,    /* a device table (waiting ring / running table / route list) is full */
+  SSB_E_INVARIANT = 4,   /* over-admission or unfinished requests (engine.py:288-292, cluster.py:159-161) */
+  SSB_E_CUDA = 5,        /* CUDA launch/runtime error                                         */
+  SSB_E_ARG = 6          /* bad arguments                                                      */
+};
+
+/* event codes of the optional event log / decision digest (engine.py:165,273-274) */
+enum { SSB_EV_ENQUEUE = 0, SSB_EV_DISPATCH = 1, SSB_EV_PREEMPT = 2, SSB_EV_PARK = 3,
+       SSB_EV_FIRST_TOKEN = 4, SSB_EV_FINISH = 5 };
+
+/* Engine parameters = EngineSettings (config.py:26-39) after build_engine()
+ * resolved the pool size, cost parameters and context window (cluster.py:28-47). */
+typedef struct {
+  int32_t policy;               /* SSB_POLICY_*                                   */
+  int32_t max_output;           /* nopreempt max_output   (policies.py:111)       */
+  double alpha;                 /* larry alpha            (policies.py:239)       */
+  double c;                     /* trail_plus c           (policies.py:163)       */
+  int32_t block_size;           /* KvBlockPool.block_size (kvmem.py:82)           */
+  int32_t pool_blocks;          /* KvBlockPool.total_blocks                       */
+  int32_t max_tokens_per_batch; /* EngineLimits           (policies.py:22-36)     */
+  int32_t max_running;          /* -1 = None (unlimited)                          */
+  int32_t max_context;          /* ModelProfile.max_context (kvmem.py:35-48)      */
+  int32_t _pad0;
+  double mem_base_s;            /* CostParams (costmodel.py:22-27)                */
+  double mem_per_kv_token_s;
+  double compute_per_token_s;
+  double overhead_s;
+} ssb_engine_params;
+
+/* One simulation instance = one run_cluster(settings, trace) call. */
+typedef struct {
+  ssb_engine_params engine;
+  int32_t n_servers;            /* ClusterSettings.n_servers (config.py:52)       */
+  int32_t balancer;             /* SSB_BAL_*                                      */
+  double poll_interval_s;       /* BalancerSettings (config.py:42-47)             */
+  double beta_prior;
+  double beta_fixed;            /* NaN = None (estimate beta)                     */
+  /* numpy PCG64 state of default_rng(ClusterSettings.seed) (cluster.py:94),
+   * taken on the host from np.random.PCG64(seed).state                          */
+  uint64_t pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo;
+  double qps_factor;            /* scale_qps divisor (workload.py:187-194); 1.0 = none */
+  int64_t trace_offset;         /* first request of this instance in the trace SoA  */
+  int64_t record_offset;        /* first request of this instance in the records SoA */
+  int64_t n_requests;
+  /* filled by ssb_prepare(): device capacities and scratch offset               */
+  int64_t scratch_offset;       /* bytes into the scratch buffer                    */
+  int32_t wait_cap;             /* waiting-ring capacity per server                 */
+  int32_t run_cap;              /* running-table capacity per server                */
+  int32_t est_cost;             /* scheduling hint (larger = start earlier)         */
+  int32_t _pad1;
+} ssb_instance;
+
+/* Trace SoA, TraceEntry (workload.py:42-56); arrivals sorted per instance. */
+typedef struct {
+  const double* arrival;
+  const int32_t* prompt;
+  const int32_t* output;
+} ssb_trace;
+
+/* Per-request results, MetricsRecord (metrics.py:20-31) + first_dispatch
+ * (time of the first `dispatch` event: queueing delay, not in the reference). */
+typedef struct {
+  double* first_token;
+  double* finish;
+  double* first_dispatch;
+  int32_t* preempt_count;
+  int32_t* server;
+} ssb_records;
+
+/* Per-instance counters (sums over the instance's engines). */
+typedef struct {
+  int64_t iterations;      /* Σ Engine.iterations (engine.py:226)                        */
+  int64_t request_steps;   /* Σ len(decode_ids)+len(prefill_chunks) per step (engine.py:300-323) */
+  int64_t batch_tokens;    /* Σ BatchPlan.total_tokens                                    */
+  int64_t dispatches;
+  int64_t preempts;        /* policy preempts + grow evictions ("preempt" events)         */
+  int64_t parks;
+  int64_t finished;
+  int64_t peak_batch_tokens; /* max Engine.peak_batch_tokens over engines                 */
+  uint64_t digest;         /* FNV-1a fold of per-engine event digests  */
+  int32_t status;          /* SSB_OK or SSB_E_*                                           */
+  int32_t _pad;
+} ssb_stats;
+
+/* Optional event log (engine.py:267-274) */
+typedef struct {
+  double time;
+  int32_t request_id;
+  int16_t server;
+  int16_t code;            /* SSB_EV_*   */
+} ssb_event;
+
+/* Summary (metrics.py:57-99) + north-star extras (TPOT, queueing delay). */
+typedef struct {
+  int64_t n_requests;
+  double ttft_p50, ttft_p95, ttft_p99;
+  double norm_ttft_p50, norm_ttft_p95;
+  double gen_time_p50, gen_time_p95;
+  double preemption_rate;
+  double throughput_rps;
+  /* extras: TPOT = (finish-first)/(output-1) over output>1 requests, queue = first_dispatch-arrival */
+  int64_t n_tpot;
+  double tpot_p50, tpot_p95, tpot_p99;
+  double queue_p50, queue_p95, queue_p99;
+  int64_t n_preempted;
+  double max_finish, min_arrival;
+} ssb_summary;
+
+/* Library/ABI identification. ssb_struct_sizes writes sizeof() of
+ * ssb_engine_params, ssb_instance, ssb_stats, ssb_event, ssb_summary,
+ * ssb_summary_group (in that order) to out[0..5]; returns 6. */
+int32_t ssb_abi_version(void);
+const char* ssb_error_string(int32_t code);
+int32_t ssb_struct_sizes(int64_t* out);
+
+/* Host-side planning: fills scratch_offset / wait_cap / run_cap of every
+ * instance (host array) and returns the scratch bytes ssb_simulate needs. */
+size_t ssb_prepare(ssb_instance* h_inst, int32_t n_inst);
+
+/* Simulate n_inst instances. h_inst: the prepared host descriptors (launch
+ * planning: instances with n_servers == 1 run one per warp in a persistent
+ * kernel, longest est_cost first; multi-server instances run one per CTA).
+ * d_inst: device copy of the same array. d_scratch: ssb_prepare() bytes.
+ * d_events (nullable): per-instance event ring of event_cap entries each,
+ * instance i writes [i*event_cap, (i+1)*event_cap); d_event_count (nullable
+ * iff d_events is) receives each instance's total event count.
+ * Returns SSB_OK once the work is enqueued; per-instance status is in d_stats. */
+int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* d_inst, int32_t n_inst,
+                     ssb_trace trace, ssb_records records, ssb_stats* d_stats,
+                     void* d_scratch, size_t scratch_bytes,
+                     ssb_event* d_events, int64_t event_cap, int64_t* d_event_count,
+                     void* stream /* cudaStream_t */);
+
+/* One summary group = one summarize(records) call (metrics.py:80-99) over
+ * records [record_offset, record_offset+n) whose trace entries are
+ * [trace_offset, trace_offset+n), arrivals divided by qps_factor.
+ * rank[0..2]: nearest ranks ceil(p/100*n) for p = 50,95,99 (metrics.py:53),
+ * computed on the host in Python float arithmetic exactly as the reference;
+ * rank[3..5]: the same for the TPOT sample size n_tpot (0 if unknown yet:
+ * ssb_summarize then derives it with the integer identity (p*n+99)/100,
+ * which equals the float form for n <= 1e7). */
+typedef struct {
+  int64_t record_offset;
+  int64_t trace_offset;
+  int64_t n;
+  double qps_factor;
+  int64_t rank[6];
+} ssb_summary_group;
+
+size_t ssb_summary_work_bytes(const ssb_summary_group* h_groups, int32_t n_groups);
+/* h_groups: host copy (launch planning); d_groups: device copy. */
+int32_t ssb_summarize(ssb_trace trace, ssb_records records,
+                      const ssb_summary_group* h_groups, const ssb_summary_group* d_groups,
+                      int32_t n_groups, ssb_summary* d_summary,
+                      void* d_work, size_t work_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSB_H_ */

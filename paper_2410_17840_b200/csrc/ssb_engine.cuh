@@ -1,0 +1,859 @@
+// ssb_engine.cuh — warp-synchronous device restatement of one serving engine.
+//
+// One warp owns one engine (replica). All 32 lanes hold identical copies of
+// the engine scalars (clock, free blocks, counts, digest ...) and cooperate on
+// the per-request work with ballots, shuffles and warp scans:
+//
+//   Engine.step            engine.py:193-234      -> Eng::step
+//   FcfsPolicy.select      policies.py:87-97      -> select_prefix (warp prefix-sum + ballot)
+//   NoPreemptPolicy        policies.py:133-146    -> select_prefix (reservation blocks)
+//   ShortestRemaining      policies.py:168-212    -> select_trail  (ordered warp argmin extraction)
+//   LoadAdaptive / LARRY   policies.py:244-276    -> select_larry  (ordered warp argmax extraction)
+//   _form_batch            engine.py:300-323      -> form_batch    (warp scan over the running table)
+//   iteration_latency      costmodel.py:37-47     -> latency (binary64, explicit __d*_rn, no FMA)
+//   _apply_progress        engine.py:325-358      -> progress      (parallel commit up to the first
+//   _grow_or_evict / _evict_for_blocks :381-412                      failing grow, serial eviction)
+//   KvBlockPool            kvmem.py:74-154        -> free_blocks + per-entry (prompt+generated)
+//
+// Data layout (per engine, in the scratch buffer, see ssb_kernels.cu):
+//   waiting ring  SoA {rid|flag, pending, key, enqueue_time}       (deque, engine.py:162)
+//   running table SoA {rid, prompt, output, generated, prefill_done, state, plan}
+//                 kept in dispatch_seq order == dict insertion order (engine.py:163,297)
+// A running request's KV allocation is always prompt+generated tokens
+// (dispatch allocates pending_prefill = prompt+generated, first-token and
+// decode grows keep that invariant), so the pool needs no per-request token map.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ssb.h"
+
+namespace ssb {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int ST_GONE = 0;     // finished / evicted / parked during this step (compacted away)
+constexpr int ST_PREFILL = 1;  // RequestState.PREFILLING
+constexpr int ST_DECODE = 2;   // RequestState.DECODING
+constexpr int FLAG_SEEN = (int)0x80000000;  // waiting entry was dispatched before (preempted/parked)
+constexpr unsigned long long FNV_OFF = 0xcbf29ce484222325ULL;
+constexpr unsigned long long FNV_PRIME = 0x100000001b3ULL;
+
+struct Cfg {
+  int policy, max_output, bs, bs_shift, pool, cap, max_running, max_ctx;
+  int n_servers, Wc, Rc;
+  double alpha, c, mem_base, mem_kv, compute, overhead, qps;
+};
+
+// Persisted per-engine state (global scratch; registers while a warp runs it).
+struct Srv {
+  double clock;
+  long long iterations, rsteps, btokens, dispatches, preempts, parks, finished, peak;
+  unsigned long long digest;
+  long long wpend_sum;       // Σ pending_prefill over waiting (snapshot_stats, cluster.py:53)
+  long long fin_in, fin_out, fin_cnt;  // completions (BetaEstimator.update, balancers.py:81-86)
+  long long enq_prompt_sum;  // Σ prompt over enqueued arrivals (inbox accounting)
+  long long ev_n;
+  long long pf_pend;         // Σ pending over PREFILLING entries
+  int free_blocks, R, W, whead, committed, next_arr, status, ndec;
+};
+
+struct SrvPtr {
+  double* w_enq;
+  int* w_rid;
+  int* w_pend;
+  int* w_key;
+  int* r_rid;
+  int* r_prompt;
+  int* r_out;
+  int* r_gen;
+  int* r_pfd;
+  int* r_st;
+  int* r_plan;
+  int* l_a;   // dispatch list (physical ring slots) / scratch list
+  int* l_b;   // preempt list (table indices) / scratch list
+  int* v_idx; // trail_plus victims sorted by (-remaining, -dispatch_seq)
+  int* v_rem;
+  long long* v_cum;
+  int* rl;    // route list (arrival ids routed to this engine), n_servers > 1
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+__device__ __forceinline__ long long warp_incl_scan_ll(long long v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long n = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+struct Eng {
+  Cfg cfg;
+  Srv st;
+  SrvPtr p;
+  const double* arrival;  // instance trace base
+  const int* prompt;
+  const int* output;
+  double* rec_ft;         // instance record base
+  double* rec_fin;
+  double* rec_fd;
+  int* rec_pc;
+  int* rec_srv;
+  ssb_event* ev;          // nullable
+  long long ev_cap;
+  int server;
+  int lane;
+
+  __device__ __forceinline__ int blocks(int tokens) const {  // kvmem.py:15-21
+    return cfg.bs_shift >= 0 ? (tokens + cfg.bs - 1) >> cfg.bs_shift : (tokens + cfg.bs - 1) / cfg.bs;
+  }
+  __device__ __forceinline__ int phys(int k) const {  // ring slot of logical position k
+    int x = st.whead + k;
+    return x >= cfg.Wc ? x - cfg.Wc : x;
+  }
+  __device__ __forceinline__ double arrival_of(int rid) const {
+    return __ddiv_rn(arrival[rid], cfg.qps);  // scale_qps (workload.py:193)
+  }
+  __device__ __forceinline__ int wkey_for(int prompt_len, int out, int gen) const {
+    if (cfg.policy == SSB_POLICY_NOPREEMPT) {  // policies.py:116-117 reservation, in blocks
+      int t = min(cfg.max_ctx, prompt_len + cfg.max_output);
+      return blocks(t);
+    }
+    return out - gen;  // trail_plus remaining output (policies.py:172)
+  }
+  __device__ __forceinline__ bool has_work() const { return st.W > 0 || st.R > 0; }
+
+  // ---- event log + decision digest (engine.py:273-274) ----
+  __device__ __forceinline__ void fold(int code, int rid) {
+    unsigned long long tb = (unsigned long long)__double_as_longlong(st.clock);
+    unsigned long long h = st.digest;
+    h ^= (unsigned long long)code; h *= FNV_PRIME;
+    h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
+    h ^= tb; h *= FNV_PRIME;
+    st.digest = h;
+  }
+  __device__ __forceinline__ void log_at(long long pos, int code, int rid) {
+    if (ev != nullptr && pos < ev_cap) {
+      ssb_event e;
+      e.time = st.clock;
+      e.request_id = rid;
+      e.server = (int16_t)server;
+      e.code = (int16_t)code;
+      ev[pos] = e;
+    }
+  }
+  // one event per lane in `mask`, lane order (warp-uniform call)
+  __device__ void emit(unsigned mask, int code, int rid_lane) {
+    if (ev != nullptr && ((mask >> lane) & 1u)) log_at(st.ev_n + __popc(mask & lanemask_lt()), code, rid_lane);
+    unsigned m = mask;
+    while (m) {
+      int b = __ffs(m) - 1;
+      m &= m - 1;
+      fold(code, __shfl_sync(FULL, rid_lane, b));
+    }
+    st.ev_n += __popc(mask);
+  }
+  // first_token (mask_a) then finish (mask_b) per lane, lanes in order
+  __device__ void emit2(unsigned mask_a, int code_a, unsigned mask_b, int code_b, int rid_lane) {
+    unsigned both = mask_a | mask_b;
+    if (ev != nullptr && ((both >> lane) & 1u)) {
+      unsigned lt = lanemask_lt();
+      long long pos = st.ev_n + __popc(mask_a & lt) + __popc(mask_b & lt);
+      if ((mask_a >> lane) & 1u) log_at(pos++, code_a, rid_lane);
+      if ((mask_b >> lane) & 1u) log_at(pos, code_b, rid_lane);
+    }
+    unsigned m = both;
+    while (m) {
+      int b = __ffs(m) - 1;
+      m &= m - 1;
+      int rid = __shfl_sync(FULL, rid_lane, b);
+      if ((mask_a >> b) & 1u) fold(code_a, rid);
+      if ((mask_b >> b) & 1u) fold(code_b, rid);
+    }
+    st.ev_n += __popc(mask_a) + __popc(mask_b);
+  }
+  __device__ __forceinline__ void emit1(int code, int rid) {  // uniform single event
+    if (lane == 0) log_at(st.ev_n, code, rid);
+    fold(code, rid);
+    st.ev_n += 1;
+  }
+
+  // ---- Engine.enqueue for every routed arrival with arrival <= clock (engine.py:175-184, 261-262) ----
+  __device__ void enqueue_ready(int n_avail) {
+    while (st.next_arr < n_avail) {
+      int k = st.next_arr + lane;
+      bool valid = k < n_avail;
+      int rid = 0;
+      bool ok = false;
+      if (valid) {
+        rid = (cfg.n_servers == 1) ? k : p.rl[k];
+        ok = arrival_of(rid) <= st.clock;
+      }
+      unsigned m = __ballot_sync(FULL, ok);  // a prefix: routes are in arrival order
+      int cnt = __popc(m);
+      if (cnt == 0) break;
+      if (st.W + cnt > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
+      int pr = 0;
+      if (ok) {
+        pr = prompt[rid];
+        int pos = phys(st.W + lane);
+        p.w_rid[pos] = rid;
+        p.w_pend[pos] = pr;
+        p.w_key[pos] = wkey_for(pr, output[rid], 0);
+        p.w_enq[pos] = st.clock;
+        rec_srv[rid] = server;
+      }
+      emit(m, SSB_EV_ENQUEUE, rid);
+      long long s = warp_sum_ll(pr);
+      st.W += cnt;
+      st.wpend_sum += s;
+      st.enq_prompt_sum += s;
+      st.next_arr += cnt;
+      if (cnt < 32) break;
+    }
+    __syncwarp();
+  }
+
+  // ---- push a running entry back to the waiting head (_preempt, engine.py:368-379) ----
+  // uniform call; the entry is table index j with loaded fields
+  __device__ void preempt_entry(int j, int rid, int pr, int out, int gen, int pfd, int state, int code) {
+    int alloc = pr + gen;  // KV tokens held
+    st.free_blocks += blocks(alloc);
+    if (state == ST_DECODE) st.ndec -= 1;
+    else st.pf_pend -= (long long)(alloc - pfd);
+    if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= wkey_for(pr, out, gen);
+    if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
+    st.whead = (st.whead == 0) ? cfg.Wc - 1 : st.whead - 1;
+    if (lane == 0) {
+      int pos = st.whead;
+      p.w_rid[pos] = rid | FLAG_SEEN;
+      p.w_pend[pos] = alloc;  // pending_prefill = prompt + generated (prefill_done reset)
+      p.w_key[pos] = wkey_for(pr, out, gen);
+      p.w_enq[pos] = st.clock;
+      p.r_st[j] = ST_GONE;
+      rec_pc[rid] += 1;
+    }
+    st.W += 1;
+    st.wpend_sum += alloc;
+    if (code == SSB_EV_PARK) st.parks += 1; else st.preempts += 1;
+    emit1(code, rid);
+    __syncwarp();
+  }
+
+  // ---- stable compaction of the running table (drops ST_GONE) ----
+  __device__ void compact_running() {
+    int out = 0;
+    for (int base = 0; base < st.R; base += 32) {
+      int j = base + lane;
+      bool valid = j < st.R;
+      int rid = 0, pr = 0, o = 0, g = 0, f = 0, s = ST_GONE;
+      if (valid) {
+        s = p.r_st[j];
+        rid = p.r_rid[j]; pr = p.r_prompt[j]; o = p.r_out[j]; g = p.r_gen[j]; f = p.r_pfd[j];
+      }
+      bool keep = valid && s != ST_GONE;
+      unsigned m = __ballot_sync(FULL, keep);
+      __syncwarp();
+      if (keep) {
+        int d = out + __popc(m & lanemask_lt());
+        p.r_rid[d] = rid; p.r_prompt[d] = pr; p.r_out[d] = o; p.r_gen[d] = g; p.r_pfd[d] = f; p.r_st[d] = s;
+      }
+      out += __popc(m);
+      __syncwarp();
+    }
+    st.R = out;
+  }
+
+  // ---- FCFS / NoPreempt: dispatch the longest fitting queue prefix ----
+  __device__ int select_prefix() {
+    long long slots = cfg.max_running < 0 ? (1LL << 40) : (long long)cfg.max_running - st.R;  // policies.py:70-73
+    int limit = (cfg.policy == SSB_POLICY_FCFS) ? st.free_blocks : cfg.pool - st.committed;
+    int D = 0, used = 0;
+    for (int base = 0; base < st.W; base += 32) {
+      int k = base + lane;
+      bool valid = k < st.W;
+      int need = 0;
+      if (valid) {
+        int pos = phys(k);
+        need = (cfg.policy == SSB_POLICY_FCFS) ? blocks(p.w_pend[pos]) : p.w_key[pos];
+      }
+      int incl = warp_incl_scan(need, lane) + used;  // cumulative blocks (need >= 1 -> monotone)
+      bool ok = valid && (long long)k < slots && incl <= limit;
+      unsigned m = __ballot_sync(FULL, ok);
+      int cnt = __popc(m);
+      D += cnt;
+      if (cnt < 32) break;
+      used = __shfl_sync(FULL, incl, 31);
+    }
+    return D;
+  }
+
+  // ---- LARRY (policies.py:244-276): ordered extraction by (-score, enqueue_time, id) ----
+  __device__ int select_larry() {
+    if (st.W == 0) return 0;
+    long long slots = cfg.max_running < 0 ? (1LL << 40) : (long long)cfg.max_running - st.R;
+    // token budget left after running work (policies.py:251-257) == max(0, max(0, cap-#decoding) - Σ pending(prefilling))
+    long long budget = (long long)cfg.cap - st.ndec;
+    if (budget < 0) budget = 0;
+    budget -= st.pf_pend;
+    if (budget < 0) budget = 0;
+    int free = st.free_blocks;
+    const long long ql = st.W;  // queue_len, fixed for the step (:259)
+    int nd = 0;
+    bool have_last = false;
+    double l_sc = 0.0, l_enq = 0.0;
+    int l_rid = 0;
+    while (true) {
+      if ((long long)nd >= slots || budget <= 0 || free <= 0) break;  // need >= 1 always
+      bool found = false;
+      double b_sc = 0.0, b_enq = 0.0;
+      int b_rid = 0x7fffffff, b_k = -1;
+      for (int k = lane; k < st.W; k += 32) {
+        int pos = phys(k);
+        int rid = p.w_rid[pos] & 0x7fffffff;
+        int pend = p.w_pend[pos];
+        double enq = p.w_enq[pos];
+        // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending
+        double sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, enq)), (double)(ql * (long long)pend));
+        if (have_last) {  // strictly after the last extracted key
+          bool after = (sc < l_sc) || (sc == l_sc && (enq > l_enq || (enq == l_enq && rid > l_rid)));
+          if (!after) continue;
+        }
+        bool better = !found || (sc > b_sc) || (sc == b_sc && (enq < b_enq || (enq == b_enq && rid < b_rid)));
+        if (better) { found = true; b_sc = sc; b_enq = enq; b_rid = rid; b_k = k; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        int of = __shfl_xor_sync(FULL, (int)found, o);
+        double osc = __shfl_xor_sync(FULL, b_sc, o);
+        double oenq = __shfl_xor_sync(FULL, b_enq, o);
+        int orid = __shfl_xor_sync(FULL, b_rid, o);
+        int ok_ = __shfl_xor_sync(FULL, b_k, o);
+        bool take = of && (!found || (osc > b_sc) ||
+                           (osc == b_sc && (oenq < b_enq || (oenq == b_enq && orid < b_rid))));
+        if (take) { found = true; b_sc = osc; b_enq = oenq; b_rid = orid; b_k = ok_; }
+      }
+      if (!found) break;
+      int pos = phys(b_k);
+      int pend = p.w_pend[pos];
+      int need = blocks(pend);
+      if (need > free) break;
+      if (lane == 0) p.l_a[nd] = pos;
+      nd++;
+      free -= need;
+      budget -= min((long long)pend, budget);
+      have_last = true; l_sc = b_sc; l_enq = b_enq; l_rid = b_rid;
+    }
+    __syncwarp();
+    return nd;
+  }
+
+  // ---- trail_plus victims: eligible running entries sorted by (-remaining, -dispatch_seq) ----
+  __device__ int build_victims() {
+    // eligible: unmarked (r_plan == 0) and generated < c * output_len (policies.py:190-196)
+    int V = 0;
+    for (int base = 0; base < st.R; base += 32) {
+      int j = base + lane;
+      bool e = false;
+      if (j < st.R) e = p.r_plan[j] == 0 && (double)p.r_gen[j] < __dmul_rn(cfg.c, (double)p.r_out[j]);
+      V += __popc(__ballot_sync(FULL, e));
+    }
+    // rank sort: rank(v) = #{u eligible : key_u > key_v}, key = (remaining << 32) | idx
+    for (int base = 0; base < st.R; base += 32) {
+      int j = base + lane;
+      bool e = false;
+      unsigned long long kv = 0;
+      int rem = 0, blk = 0;
+      if (j < st.R) {
+        e = p.r_plan[j] == 0 && (double)p.r_gen[j] < __dmul_rn(cfg.c, (double)p.r_out[j]);
+        rem = p.r_out[j] - p.r_gen[j];
+        blk = blocks(p.r_prompt[j] + p.r_gen[j]);
+        kv = ((unsigned long long)(unsigned)rem << 32) | (unsigned)j;
+      }
+      if (e) {
+        int rank = 0;
+        for (int u = 0; u < st.R; ++u) {
+          if (p.r_plan[u] != 0) continue;
+          int gu = p.r_gen[u], ou = p.r_out[u];
+          if (!((double)gu < __dmul_rn(cfg.c, (double)ou))) continue;
+          unsigned long long ku = ((unsigned long long)(unsigned)(ou - gu) << 32) | (unsigned)u;
+          rank += ku > kv;
+        }
+        p.v_idx[rank] = j;
+        p.v_rem[rank] = rem;
+        p.v_cum[rank] = blk;  // prefix-summed below
+      }
+    }
+    __syncwarp();
+    long long carry = 0;
+    for (int base = 0; base < V; base += 32) {
+      int i = base + lane;
+      long long b = i < V ? p.v_cum[i] : 0;
+      long long incl = warp_incl_scan_ll(b, lane) + carry;
+      if (i < V) p.v_cum[i] = incl;
+      carry = __shfl_sync(FULL, incl, 31);
+    }
+    __syncwarp();
+    return V;
+  }
+  // number of victims with remaining > r (a prefix of the sorted list)
+  __device__ __forceinline__ int victims_above(int V, int r) const {
+    int lo = 0, hi = V;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (p.v_rem[mid] > r) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  }
+
+  // ---- trail_plus (policies.py:168-212): greedy skip in (remaining, arrival, id) order ----
+  // arrival order == id order (trace sorted, ids in trace order), so the key is (remaining, id).
+  __device__ void select_trail(int& nd_out, int& np_out) {
+    int nd = 0, np = 0;
+    if (st.W == 0) { nd_out = np_out = 0; return; }
+    const bool can_preempt = cfg.c != 0.0;
+    if (can_preempt)
+      for (int j = lane; j < st.R; j += 32) p.r_plan[j] = 0;  // marks
+    __syncwarp();
+    int free = st.free_blocks;
+    unsigned long long last = 0;  // keys are >= 1<<32 (remaining >= 1)
+    int V = -1;
+    while (true) {
+      if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;
+      if (can_preempt && V < 0) V = build_victims();
+      unsigned long long best = ~0ULL;
+      int best_k = -1;
+      for (int k = lane; k < st.W; k += 32) {
+        int pos = phys(k);
+        int rid = p.w_rid[pos] & 0x7fffffff;
+        int rem = p.w_key[pos];
+        unsigned long long key = ((unsigned long long)(unsigned)rem << 32) | (unsigned)rid;
+        if (key <= last || key >= best) continue;
+        int need = blocks(p.w_pend[pos]);
+        bool ok = need <= free;
+        if (!ok && can_preempt) {
+          int m = victims_above(V, rem);
+          long long gain = m > 0 ? p.v_cum[m - 1] : 0;
+          ok = (long long)free + gain >= need;
+        }
+        if (ok) { best = key; best_k = k; }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+        int ok_ = __shfl_xor_sync(FULL, best_k, o);
+        if (ob < best) { best = ob; best_k = ok_; }
+      }
+      if (best == ~0ULL) break;
+      int pos = phys(best_k);
+      int need = blocks(p.w_pend[pos]);
+      int rem = (int)(best >> 32);
+      if (need > free) {
+        // take victims (largest remaining first, youngest first on ties) until free+gain >= need
+        int m = victims_above(V, rem);
+        long long gain = 0;
+        int taken = 0;
+        while (taken < m && (long long)free + gain < need) {
+          gain = p.v_cum[taken];
+          taken++;
+        }
+        for (int t = lane; t < taken; t += 32) {
+          int j = p.v_idx[t];
+          p.r_plan[j] = 1;  // marked
+          p.l_b[np + t] = j;
+        }
+        np += taken;
+        free += (int)gain;
+        V = -1;  // marks changed: rebuild before the next candidate
+        __syncwarp();
+      }
+      if (lane == 0) p.l_a[nd] = pos;
+      nd++;
+      free -= need;
+      last = best;
+    }
+    __syncwarp();
+    nd_out = nd;
+    np_out = np;
+  }
+
+  // ---- remove dispatched entries (physical slots in l_a[0..nd)) from an unordered waiting set ----
+  __device__ void remove_dispatched_unordered(int nd) {
+    for (int i = lane; i < nd; i += 32) p.w_rid[p.l_a[i]] = -1;
+    __syncwarp();
+    int Wn = st.W - nd;
+    // holes: dispatched slots at logical position < Wn ; movers: kept entries at logical >= Wn
+    int nh = 0;
+    for (int base = 0; base < nd; base += 32) {
+      int i = base + lane;
+      bool h = false;
+      int lg = 0;
+      if (i < nd) {
+        lg = p.l_a[i] - st.whead;
+        if (lg < 0) lg += cfg.Wc;
+        h = lg < Wn;
+      }
+      unsigned m = __ballot_sync(FULL, h);
+      if (h) p.l_b[nh + __popc(m & lanemask_lt())] = p.l_a[i];
+      nh += __popc(m);
+    }
+    __syncwarp();
+    int nm = 0;
+    for (int base = Wn; base < st.W; base += 32) {
+      int k = base + lane;
+      bool mv = false;
+      int pos = 0;
+      if (k < st.W) {
+        pos = phys(k);
+        mv = p.w_rid[pos] != -1;
+      }
+      unsigned m = __ballot_sync(FULL, mv);
+      if (mv) {
+        int h = p.l_b[nm + __popc(m & lanemask_lt())];
+        p.w_rid[h] = p.w_rid[pos];
+        p.w_pend[h] = p.w_pend[pos];
+        p.w_key[h] = p.w_key[pos];
+        p.w_enq[h] = p.w_enq[pos];
+      }
+      nm += __popc(m);
+    }
+    if (nm != nh) st.status = SSB_E_INVARIANT;
+    st.W = Wn;
+    __syncwarp();
+  }
+
+  // ---- apply dispatches (engine.py:287-298) in decision order ----
+  __device__ void apply_dispatches(int nd, bool prefix_mode) {
+    if (nd == 0) return;
+    if (st.R + nd > cfg.Rc) { st.status = SSB_E_CAPACITY; return; }
+    int need_sum = 0;
+    long long pend_sum = 0;
+    int res_sum = 0;
+    for (int base = 0; base < nd; base += 32) {
+      int j = base + lane;
+      bool valid = j < nd;
+      int rid = 0;
+      if (valid) {
+        int pos = prefix_mode ? phys(j) : p.l_a[j];
+        int wr = p.w_rid[pos];
+        rid = wr & 0x7fffffff;
+        int pend = p.w_pend[pos];
+        int pr = prompt[rid];
+        int t = st.R + j;
+        p.r_rid[t] = rid;
+        p.r_prompt[t] = pr;
+        p.r_out[t] = output[rid];
+        p.r_gen[t] = pend - pr;
+        p.r_pfd[t] = 0;
+        p.r_st[t] = ST_PREFILL;
+        if (!(wr & FLAG_SEEN)) rec_fd[rid] = st.clock;  // first dispatch (queueing delay)
+        need_sum += blocks(pend);
+        pend_sum += pend;
+        if (cfg.policy == SSB_POLICY_NOPREEMPT) res_sum += p.w_key[pos];
+      }
+      emit(__ballot_sync(FULL, valid), SSB_EV_DISPATCH, rid);
+    }
+    need_sum = warp_sum(need_sum);
+    pend_sum = warp_sum_ll(pend_sum);
+    res_sum = warp_sum(res_sum);
+    st.free_blocks -= need_sum;  // try_allocate (kvmem.py:106-117)
+    if (st.free_blocks < 0) st.status = SSB_E_INVARIANT;  // "policy over-admitted" (engine.py:288-292)
+    st.committed += res_sum;
+    st.wpend_sum -= pend_sum;
+    st.pf_pend += pend_sum;
+    st.R += nd;
+    st.dispatches += nd;
+    __syncwarp();
+    if (prefix_mode) {
+      st.whead = phys(nd);
+      st.W -= nd;
+    } else {
+      remove_dispatched_unordered(nd);
+    }
+  }
+
+  // ---- _form_batch (engine.py:300-323) + resident KV (engine.py:217-218) ----
+  // writes r_plan: 1 = decode token, >1 = prefill chunk + 1, 0 = not in the plan.
+  // prefill plan entries are also listed (table index) in l_b[0..npf).
+  __device__ void form_batch(int& total, long long& resident, int& nentries, int& npf) {
+    const int cap = cfg.cap;
+    int n_dec_plan = min(st.ndec, cap);
+    int budget = cap - n_dec_plan;
+    int dec_seen = 0, pf_used = 0, npf_ = 0;
+    long long res = 0;
+    for (int base = 0; base < st.R; base += 32) {
+      int j = base + lane;
+      bool valid = j < st.R;
+      int s = ST_GONE, pr = 0, g = 0, f = 0;
+      if (valid) { s = p.r_st[j]; pr = p.r_prompt[j]; g = p.r_gen[j]; f = p.r_pfd[j]; }
+      bool dec = s == ST_DECODE;
+      bool pf = s == ST_PREFILL;
+      unsigned md = __ballot_sync(FULL, dec);
+      int drank = dec_seen + __popc(md & lanemask_lt());
+      bool in_dec = dec && drank < cap;
+      int pend = pf ? pr + g - f : 0;
+      int incl = warp_incl_scan(pend, lane) + pf_used;
+      int before = incl - pend;  // prefill tokens claimed before this entry
+      int chunk = 0;
+      if (pf && budget - before > 0) chunk = min(pend, budget - before);
+      bool in_pf = chunk > 0;
+      int plan = in_dec ? 1 : (in_pf ? chunk + 1 : 0);
+      if (valid) p.r_plan[j] = plan;
+      unsigned mp = __ballot_sync(FULL, in_pf);
+      if (in_pf) p.l_b[npf_ + __popc(mp & lanemask_lt())] = j;
+      npf_ += __popc(mp);
+      long long ctx = in_dec ? (long long)(pr + g) : (in_pf ? (long long)f : 0);
+      res += ctx;
+      dec_seen += __popc(md);
+      pf_used = __shfl_sync(FULL, incl, 31);
+    }
+    res = warp_sum_ll(res);
+    int pf_tokens = (int)min((long long)budget, (long long)pf_used);
+    total = n_dec_plan + pf_tokens;
+    resident = res;
+    nentries = n_dec_plan + npf_;
+    npf = npf_;
+    __syncwarp();
+  }
+
+  // ---- _apply_progress (engine.py:325-358) ----
+  // Lanes evaluate their grow (kvmem.py:119-140) against the running free count
+  // (exclusive scan of released-minus-grown blocks); every lane before the first
+  // failing grow commits in parallel; the failing one runs the serial eviction
+  // cascade (_grow_or_evict / _evict_for_blocks) and the chunk restarts after it.
+  template <bool PREFILL>
+  __device__ void progress_group(int j_lane, bool in_group, bool& removed_any) {
+    int start = 0;
+    while (true) {
+      int rid = 0, pr = 0, out = 0, g = 0, f = 0, s = ST_GONE, plan = 0;
+      bool act = in_group && lane >= start;
+      if (act) {
+        s = p.r_st[j_lane];
+        act = s == (PREFILL ? ST_PREFILL : ST_DECODE);  // skip entries evicted earlier in this pass
+      }
+      if (act) {
+        rid = p.r_rid[j_lane]; pr = p.r_prompt[j_lane]; out = p.r_out[j_lane]; g = p.r_gen[j_lane];
+        f = p.r_pfd[j_lane]; plan = p.r_plan[j_lane];
+      }
+      int f2 = f, extra = 0, rel = 0;
+      bool grow = false, fin = false, first = false, recompute = false;
+      if (act) {
+        if (PREFILL) {
+          f2 = f + (plan - 1);
+          bool complete = f2 >= pr + g;
+          first = complete && g == 0;
+          recompute = complete && g > 0;
+          grow = first;
+          if (first) {
+            extra = blocks(pr + 1) - blocks(pr);
+            fin = out == 1;
+            rel = fin ? blocks(pr + 1) : 0;
+          }
+        } else {
+          grow = true;
+          int cur = pr + g;
+          extra = blocks(cur + 1) - blocks(cur);
+          fin = g + 1 == out;
+          rel = fin ? blocks(cur + 1) : 0;
+        }
+      }
+      int d = act ? rel - extra : 0;
+      int excl = warp_incl_scan(d, lane) - d;
+      bool fail = act && grow && extra > st.free_blocks + excl;
+      unsigned mf = __ballot_sync(FULL, fail);
+      int fl = mf ? __ffs(mf) - 1 : 32;
+      bool commit = act && lane < fl;
+      // commit lanes [start, fl)
+      unsigned m_first = __ballot_sync(FULL, commit && first);
+      unsigned m_fin = __ballot_sync(FULL, commit && fin);
+      unsigned m_dec_in = __ballot_sync(FULL, commit && (first || recompute));
+      if (commit) {
+        if (PREFILL) {
+          p.r_pfd[j_lane] = f2;
+          if (first) {
+            p.r_gen[j_lane] = 1;
+            rec_ft[rid] = st.clock;
+          }
+          if (first || recompute) p.r_st[j_lane] = fin ? ST_GONE : ST_DECODE;
+        } else {
+          p.r_gen[j_lane] = g + 1;
+          if (fin) p.r_st[j_lane] = ST_GONE;
+        }
+        if (fin) rec_fin[rid] = st.clock;
+      }
+      int dsum = __shfl_sync(FULL, excl + d, 31);  // total over all lanes...
+      // ...but only lanes < fl commit: take the exclusive prefix at fl
+      int dcommit = (fl == 32) ? dsum : __shfl_sync(FULL, excl, fl & 31);
+      st.free_blocks += dcommit;
+      if (PREFILL) {
+        int chunk_sum = warp_sum(commit ? plan - 1 : 0);
+        st.pf_pend -= chunk_sum;
+        if (PREFILL) emit2(m_first, SSB_EV_FIRST_TOKEN, m_fin, SSB_EV_FINISH, rid);
+      } else {
+        emit(m_fin, SSB_EV_FINISH, rid);
+      }
+      int n_fin = __popc(m_fin);
+      st.ndec += __popc(m_dec_in) - n_fin;
+      if (n_fin) {
+        removed_any = true;
+        st.finished += n_fin;
+        st.fin_cnt += n_fin;
+        st.fin_in += warp_sum(commit && fin ? pr : 0);
+        st.fin_out += warp_sum(commit && fin ? out : 0);
+        if (cfg.policy == SSB_POLICY_NOPREEMPT)
+          st.committed -= warp_sum(commit && fin ? wkey_for(pr, out, 0) : 0);
+      }
+      __syncwarp();
+      if (fl == 32) break;
+      // ---- serial slow path for lane fl: its grow does not fit ----
+      removed_any = true;
+      int j = __shfl_sync(FULL, j_lane, fl);
+      int frid = __shfl_sync(FULL, rid, fl), fpr = __shfl_sync(FULL, pr, fl), fout = __shfl_sync(FULL, out, fl);
+      int fg = __shfl_sync(FULL, g, fl), ff2 = __shfl_sync(FULL, f2, fl), fext = __shfl_sync(FULL, extra, fl);
+      bool ffin = __shfl_sync(FULL, (int)fin, fl) != 0;
+      if (PREFILL && lane == 0) p.r_pfd[j] = ff2;  // the chunk landed before the grow
+      if (PREFILL) st.pf_pend -= (long long)(ff2 - __shfl_sync(FULL, f, fl));
+      __syncwarp();
+      // _evict_for_blocks: youngest dispatch first (table order descending), skipping the grower
+      int needed = fext;  // blocks(new) - allocated_blocks(r)
+      for (int base = ((st.R - 1) >> 5) << 5; base >= 0 && st.free_blocks < needed; base -= 32) {
+        int v = base + lane;
+        bool live = v < st.R && v != j && p.r_st[v] != ST_GONE;
+        unsigned ml = __ballot_sync(FULL, live);
+        while (ml && st.free_blocks < needed) {
+          int b = 31 - __clz(ml);
+          ml &= ~(1u << b);
+          int vj = base + b;
+          int vs = p.r_st[vj];
+          int vrid = p.r_rid[vj], vpr = p.r_prompt[vj], vout = p.r_out[vj], vg = p.r_gen[vj], vf = p.r_pfd[vj];
+          preempt_entry(vj, vrid, vpr, vout, vg, vf, vs, SSB_EV_PREEMPT);
+        }
+      }
+      if (st.free_blocks >= needed) {  // retry succeeds
+        st.free_blocks -= fext;
+        if (PREFILL) {
+          if (lane == 0) { p.r_gen[j] = 1; rec_ft[frid] = st.clock; p.r_st[j] = ffin ? ST_GONE : ST_DECODE; }
+          emit1(SSB_EV_FIRST_TOKEN, frid);
+          st.ndec += 1;
+        } else {
+          if (lane == 0) { p.r_gen[j] = fg + 1; if (ffin) p.r_st[j] = ST_GONE; }
+        }
+        if (ffin) {
+          if (lane == 0) rec_fin[frid] = st.clock;
+          st.free_blocks += PREFILL ? blocks(fpr + 1) : blocks(fpr + fg + 1);
+          emit1(SSB_EV_FINISH, frid);
+          st.ndec -= 1;
+          st.finished += 1; st.fin_cnt += 1; st.fin_in += fpr; st.fin_out += fout;
+          if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= wkey_for(fpr, fout, 0);
+        }
+      } else {  // park: the grower alone exceeds the pool (engine.py:403-412)
+        preempt_entry(j, frid, fpr, fout, fg, ff2, PREFILL ? ST_PREFILL : ST_DECODE, SSB_EV_PARK);
+      }
+      __syncwarp();
+      start = fl + 1;
+      if (start >= 32) break;
+    }
+  }
+
+  __device__ bool progress(int npf) {
+    bool removed = false;
+    // prefill chunks in plan order (table indices listed in l_b)
+    for (int base = 0; base < npf; base += 32) {
+      int i = base + lane;
+      int j = i < npf ? p.l_b[i] : 0;
+      progress_group<true>(j, i < npf, removed);
+    }
+    // then decode tokens in plan order
+    for (int base = 0; base < st.R; base += 32) {
+      int j = base + lane;
+      bool in = j < st.R && p.r_plan[j] == 1;
+      progress_group<false>(j, in, removed);
+    }
+    return removed;
+  }
+
+  // ---- Engine.step (engine.py:193-234) ----
+  __device__ void step() {
+    if (!has_work()) { st.status = SSB_E_STALL; return; }
+    int nd = 0, np = 0;
+    bool prefix = false;
+    switch (cfg.policy) {
+      case SSB_POLICY_FCFS:
+      case SSB_POLICY_NOPREEMPT: nd = select_prefix(); prefix = true; break;
+      case SSB_POLICY_TRAIL_PLUS: select_trail(nd, np); break;
+      case SSB_POLICY_LARRY: nd = select_larry(); break;
+      default: st.status = SSB_E_ARG; return;
+    }
+    if (np > 0) {  // policy preempts first (engine.py:203-204), in decision order
+      for (int t = 0; t < np; ++t) {
+        int j = p.l_b[t];
+        int vs = p.r_st[j], vrid = p.r_rid[j], vpr = p.r_prompt[j], vout = p.r_out[j], vg = p.r_gen[j],
+            vf = p.r_pfd[j];
+        preempt_entry(j, vrid, vpr, vout, vg, vf, vs, SSB_EV_PREEMPT);
+      }
+      compact_running();
+    }
+    apply_dispatches(nd, prefix);  // then dispatches (engine.py:205-206)
+    if (st.status) return;
+    int total, nent, npf;
+    long long resident;
+    form_batch(total, resident, nent, npf);
+    if (total == 0) { st.status = SSB_E_STALL; return; }  // engine.py:209-214
+    st.rsteps += nent;
+    st.btokens += total;
+    // iteration_latency (costmodel.py:45-47) then clock += latency (engine.py:219-220)
+    double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, (double)resident));
+    double comp = __dmul_rn(cfg.compute, (double)total);
+    double lat = __dadd_rn(cfg.overhead, comp > mem ? comp : mem);
+    st.clock = __dadd_rn(st.clock, lat);
+    bool removed = progress(npf);
+    if (removed) compact_running();
+    if (total > st.peak) st.peak = total;
+    st.iterations += 1;
+  }
+
+  // ---- advance: process every boundary with time < t_lim (cluster.py:142-157 / engine.py:256-265) ----
+  __device__ void advance(double t_lim, int n_avail) {
+    while (st.status == SSB_OK) {
+      double nb;
+      if (!has_work()) {
+        if (st.next_arr >= n_avail) break;  // idle until the next routed arrival
+        int rid = (cfg.n_servers == 1) ? st.next_arr : p.rl[st.next_arr];
+        double a = arrival_of(rid);
+        nb = a > st.clock ? a : st.clock;  // wake = max(t, clock) (cluster.py:139)
+      } else {
+        nb = st.clock;
+      }
+      if (!(nb < t_lim)) break;  // ties: arrivals before boundaries (cluster.py:62)
+      st.clock = nb;             // advance_to (engine.py:186-191)
+      enqueue_ready(n_avail);
+      if (st.status) break;
+      step();
+    }
+  }
+};
+
+}  // namespace ssb

@@ -1,0 +1,567 @@
+// ssb_kernels.cu — sm_100a simulation kernels + the C ABI of include/ssb.h.
+//
+//   k_engines : persistent, one warp per single-server instance (run_cluster
+//               with n_servers == 1 == Engine.run, engine.py:236-265). Warps
+//               pull instances from an atomic queue, longest first.
+//   k_cluster : one CTA per multi-server instance (run_cluster, cluster.py:65-174).
+//               Warp 0 routes arrivals (balancers.py:132-216, incl. numpy PCG64
+//               Generator.integers); every warp advances its replicas between
+//               routing barriers. Barriers are only needed where a route reads
+//               engine state: at poll instants (p2c, sal) and for sal routes
+//               whose argmin depends on beta. See DESIGN.md §cluster.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ssb_engine.cuh"
+
+using namespace ssb;
+
+namespace {
+
+constexpr int ENGINE_WARPS_PER_CTA = 4;
+
+__host__ __device__ inline long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  long long srv, w_enq, w_rid, w_pend, w_key, r_rid, r_prompt, r_out, r_gen, r_pfd, r_st, r_plan, l_a, l_b, v_idx,
+      v_rem, v_cum, rl, total;
+};
+
+__host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers) {
+  Layout L;
+  long long o = 0;
+  L.srv = o;      o = align_up(o + (long long)sizeof(Srv), 64);
+  L.w_enq = o;    o = align_up(o + 8 * Wc, 64);
+  L.w_rid = o;    o = align_up(o + 4 * Wc, 64);
+  L.w_pend = o;   o = align_up(o + 4 * Wc, 64);
+  L.w_key = o;    o = align_up(o + 4 * Wc, 64);
+  L.r_rid = o;    o = align_up(o + 4 * Rc, 64);
+  L.r_prompt = o; o = align_up(o + 4 * Rc, 64);
+  L.r_out = o;    o = align_up(o + 4 * Rc, 64);
+  L.r_gen = o;    o = align_up(o + 4 * Rc, 64);
+  L.r_pfd = o;    o = align_up(o + 4 * Rc, 64);
+  L.r_st = o;     o = align_up(o + 4 * Rc, 64);
+  L.r_plan = o;   o = align_up(o + 4 * Rc, 64);
+  L.l_a = o;      o = align_up(o + 4 * Rc, 64);
+  L.l_b = o;      o = align_up(o + 4 * Rc, 64);
+  L.v_idx = o;    o = align_up(o + 4 * Rc, 64);
+  L.v_rem = o;    o = align_up(o + 4 * Rc, 64);
+  L.v_cum = o;    o = align_up(o + 8 * Rc, 64);
+  L.rl = o;       o = align_up(o + (n_servers > 1 ? 4 * N : 0), 64);
+  L.total = align_up(o, 256);
+  return L;
+}
+
+__device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
+  SrvPtr p;
+  p.w_enq = (double*)(base + L.w_enq);
+  p.w_rid = (int*)(base + L.w_rid);
+  p.w_pend = (int*)(base + L.w_pend);
+  p.w_key = (int*)(base + L.w_key);
+  p.r_rid = (int*)(base + L.r_rid);
+  p.r_prompt = (int*)(base + L.r_prompt);
+  p.r_out = (int*)(base + L.r_out);
+  p.r_gen = (int*)(base + L.r_gen);
+  p.r_pfd = (int*)(base + L.r_pfd);
+  p.r_st = (int*)(base + L.r_st);
+  p.r_plan = (int*)(base + L.r_plan);
+  p.l_a = (int*)(base + L.l_a);
+  p.l_b = (int*)(base + L.l_b);
+  p.v_idx = (int*)(base + L.v_idx);
+  p.v_rem = (int*)(base + L.v_rem);
+  p.v_cum = (long long*)(base + L.v_cum);
+  p.rl = (int*)(base + L.rl);
+  return p;
+}
+
+__device__ inline Cfg make_cfg(const ssb_instance& I) {
+  Cfg c;
+  const ssb_engine_params& e = I.engine;
+  c.policy = e.policy;
+  c.max_output = e.max_output;
+  c.bs = e.block_size;
+  c.bs_shift = (e.block_size & (e.block_size - 1)) == 0 ? __ffs(e.block_size) - 1 : -1;
+  c.pool = e.pool_blocks;
+  c.cap = e.max_tokens_per_batch;
+  c.max_running = e.max_running;
+  c.max_ctx = e.max_context;
+  c.n_servers = I.n_servers;
+  c.Wc = I.wait_cap;
+  c.Rc = I.run_cap;
+  c.alpha = e.alpha;
+  c.c = e.c;
+  c.mem_base = e.mem_base_s;
+  c.mem_kv = e.mem_per_kv_token_s;
+  c.compute = e.compute_per_token_s;
+  c.overhead = e.overhead_s;
+  c.qps = I.qps_factor;
+  return c;
+}
+
+__device__ inline void init_srv(Srv& s, const Cfg& c) {
+  s.clock = 0.0;
+  s.iterations = s.rsteps = s.btokens = s.dispatches = s.preempts = s.parks = s.finished = s.peak = 0;
+  s.digest = FNV_OFF;
+  s.wpend_sum = s.fin_in = s.fin_out = s.fin_cnt = s.enq_prompt_sum = s.ev_n = s.pf_pend = 0;
+  s.free_blocks = c.pool;
+  s.R = s.W = s.whead = s.committed = s.next_arr = s.status = s.ndec = 0;
+}
+
+__device__ inline void bind_engine(Eng& E, const ssb_instance& I, const Cfg& cfg, unsigned char* scratch, int server,
+                                   const Layout& L, ssb_trace tr, ssb_records rec, ssb_event* ev, long long ev_cap) {
+  E.cfg = cfg;
+  E.p = make_ptrs(scratch + I.scratch_offset + (long long)server * L.total, L);
+  E.arrival = tr.arrival + I.trace_offset;
+  E.prompt = tr.prompt + I.trace_offset;
+  E.output = tr.output + I.trace_offset;
+  E.rec_ft = rec.first_token + I.record_offset;
+  E.rec_fin = rec.finish + I.record_offset;
+  E.rec_fd = rec.first_dispatch + I.record_offset;
+  E.rec_pc = rec.preempt_count + I.record_offset;
+  E.rec_srv = rec.server + I.record_offset;
+  // event ring: instance slice split evenly between the instance's servers;
+  // unused entries keep code -1 (filled by fill_events)
+  const long long slice = ev_cap / (I.n_servers > 0 ? I.n_servers : 1);
+  E.ev = ev ? ev + (long long)server * slice : nullptr;
+  E.ev_cap = slice;
+  E.server = server;
+  E.lane = lane_id();
+}
+
+__device__ inline void fill_events(const Eng& E, int lane_base, int stride) {
+  if (!E.ev) return;
+  for (long long i = lane_base; i < E.ev_cap; i += stride) {
+    ssb_event e;
+    e.time = 0.0;
+    e.request_id = -1;
+    e.server = (int16_t)E.server;
+    e.code = -1;
+    E.ev[i] = e;
+  }
+}
+
+__device__ inline void clear_records(const Eng& E, long long N, int lane_base, int stride) {
+  for (long long i = lane_base; i < N; i += stride) {
+    E.rec_ft[i] = __longlong_as_double(0x7ff8000000000000LL);
+    E.rec_fin[i] = __longlong_as_double(0x7ff8000000000000LL);
+    E.rec_fd[i] = __longlong_as_double(0x7ff8000000000000LL);
+    E.rec_pc[i] = 0;
+    E.rec_srv[i] = -1;
+  }
+}
+
+// ------------------------------------------------------------------------
+// single-server instances: one warp each, persistent
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA)
+k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, int n_order,
+          int* __restrict__ queue, ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
+          unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap, int64_t* ev_count) {
+  const int lane = lane_id();
+  while (true) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(queue, 1);
+    q = __shfl_sync(FULL, q, 0);
+    if (q >= n_order) break;
+    const int idx = order[q];
+    const ssb_instance I = inst[idx];
+    const Cfg cfg = make_cfg(I);
+    const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers);
+    Eng E;
+    bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap);
+    clear_records(E, I.n_requests, lane, 32);
+    fill_events(E, lane, 32);
+    init_srv(E.st, cfg);
+    __syncwarp();
+    E.advance(__longlong_as_double(0x7ff0000000000000LL), (int)I.n_requests);  // t_lim = +inf
+    if (E.st.status == SSB_OK && (E.st.finished != I.n_requests || E.has_work())) E.st.status = SSB_E_INVARIANT;
+    if (lane == 0) {
+      ssb_stats s;
+      s.iterations = E.st.iterations;
+      s.request_steps = E.st.rsteps;
+      s.batch_tokens = E.st.btokens;
+      s.dispatches = E.st.dispatches;
+      s.preempts = E.st.preempts;
+      s.parks = E.st.parks;
+      s.finished = E.st.finished;
+      s.peak_batch_tokens = E.st.peak;
+      unsigned long long h = FNV_OFF;
+      h ^= E.st.digest; h *= FNV_PRIME;
+      s.digest = h;
+      s.status = E.st.status;
+      s._pad = 0;
+      stats[idx] = s;
+      if (ev_count) ev_count[idx] = E.st.ev_n;
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------------
+// numpy PCG64 (XSL-RR 128/64) + Generator.integers (32-bit Lemire, buffered
+// next_uint32: low half first) — bit-exact with np.random.default_rng(seed)
+// ------------------------------------------------------------------------
+struct Pcg {
+  unsigned long long shi, slo, ihi, ilo;
+  unsigned buf;
+  int has;
+  __device__ unsigned long long next64() {
+    const unsigned long long MHI = 0x2360ED051FC65DA4ULL, MLO = 0x4385DF649FCCF645ULL;
+    unsigned long long lo = slo * MLO;
+    unsigned long long hi = __umul64hi(slo, MLO) + slo * MHI + shi * MLO;
+    unsigned long long nlo = lo + ilo;
+    hi += ihi + (nlo < lo ? 1ULL : 0ULL);
+    slo = nlo;
+    shi = hi;
+    unsigned rot = (unsigned)(shi >> 58);
+    unsigned long long x = shi ^ slo;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  __device__ unsigned next32() {
+    if (has) { has = 0; return buf; }
+    unsigned long long v = next64();
+    has = 1;
+    buf = (unsigned)(v >> 32);
+    return (unsigned)v;
+  }
+  __device__ int integers(int high) {  // [0, high)
+    unsigned rng = (unsigned)(high - 1);
+    if (rng == 0) return 0;
+    unsigned excl = rng + 1u;
+    unsigned long long m = (unsigned long long)next32() * excl;
+    unsigned left = (unsigned)m;
+    if (left < excl) {
+      unsigned thr = (0xFFFFFFFFu - rng) % excl;
+      while (left < thr) {
+        m = (unsigned long long)next32() * excl;
+        left = (unsigned)m;
+      }
+    }
+    return (int)(m >> 32);
+  }
+};
+
+// ------------------------------------------------------------------------
+// multi-server instances: one CTA each
+// ------------------------------------------------------------------------
+struct ClusterShared {
+  double t_lim;
+  double last_poll;
+  double beta;
+  int k;
+  int done;
+  int synced;
+  int err;
+};
+
+constexpr int CLUSTER_MAX_WARPS = 8;
+
+__global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr,
+                          ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch,
+                          ssb_event* events, long long ev_cap, int64_t* ev_count) {
+  extern __shared__ long long smem_ll[];
+  __shared__ ClusterShared S;
+  const int idx = order[blockIdx.x];
+  const ssb_instance I = inst[idx];
+  const int n = I.n_servers;
+  const long long N = I.n_requests;
+  long long* v_q = smem_ll;            // BalancerView.stats[s].queued_tokens
+  long long* v_f = smem_ll + n;        // .free_mem_tokens
+  long long* v_if = smem_ll + 2 * n;   // .in_flight
+  long long* rps = smem_ll + 3 * n;    // Σ prompt routed to s
+  int* cnt = (int*)(smem_ll + 4 * n);  // arrivals routed to s
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+  const Cfg cfg = make_cfg(I);
+  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n);
+  ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
+
+  // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
+  for (int s = warp; s < n; s += nwarps) {
+    Eng E;
+    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap);
+    init_srv(E.st, cfg);
+    fill_events(E, lane, 32);
+    if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
+  }
+  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+    v_q[s] = 0;
+    v_f[s] = (long long)cfg.pool * cfg.bs;
+    v_if[s] = 0;
+    rps[s] = 0;
+    cnt[s] = 0;
+  }
+  {
+    Eng E;
+    bind_engine(E, I, cfg, scratch, 0, L, tr, rec, evb, ev_cap);
+    clear_records(E, N, threadIdx.x, blockDim.x);
+  }
+  if (threadIdx.x == 0) {
+    S.k = 0; S.done = 0; S.synced = 1; S.err = 0;
+    S.last_poll = 0.0;
+    S.beta = I.beta_prior;
+  }
+  __syncthreads();
+
+  const bool uses_view = I.balancer == SSB_BAL_P2C || I.balancer == SSB_BAL_SAL;
+  const bool est_beta = I.balancer == SSB_BAL_SAL && isnan(I.beta_fixed);
+  Pcg rng;
+  rng.shi = I.pcg_state_hi; rng.slo = I.pcg_state_lo; rng.ihi = I.pcg_inc_hi; rng.ilo = I.pcg_inc_lo;
+  rng.has = 0; rng.buf = 0;
+  long long rr = 0;
+  const double* arr = tr.arrival + I.trace_offset;
+  const int* prm = tr.prompt + I.trace_offset;
+  int* rec_srv = rec.server + I.record_offset;
+  const double poll = I.poll_interval_s;
+
+  while (true) {
+    // ---------------- routing phase (warp 0) ----------------
+    if (warp == 0) {
+      int k = S.k;
+      int synced = S.synced;
+      double last_poll = S.last_poll;
+      const double beta = isnan(I.beta_fixed) ? S.beta : I.beta_fixed;
+      while (k < N) {
+        const double t = __ddiv_rn(arr[k], I.qps_factor);
+        const int pr = prm[k];
+        if (uses_view && __dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
+          if (!synced) break;
+          // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
+          for (int s = lane; s < n; s += 32) {
+            const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
+            v_q[s] = sv->wpend_sum + (rps[s] - sv->enq_prompt_sum);
+            v_f[s] = (long long)sv->free_blocks * cfg.bs;
+            v_if[s] = (long long)sv->W + sv->R + (cnt[s] - sv->next_arr);
+          }
+          __syncwarp();
+          last_poll = t;
+        }
+        int s = 0;
+        if (I.balancer == SSB_BAL_RR) {  // balancers.py:139-142
+          s = (int)(rr % n);
+          rr++;
+        } else if (I.balancer == SSB_BAL_RANDOM) {  // :152-153
+          s = rng.integers(n);
+        } else if (I.balancer == SSB_BAL_P2C) {  // :167-176
+          if (n > 1) {
+            int i = rng.integers(n);
+            int j = rng.integers(n - 1);
+            if (j >= i) j += 1;
+            s = v_if[j] < v_if[i] ? j : i;
+          }
+        } else {  // SAL (:204-212)
+          if (est_beta && !synced) {
+            // the argmin is beta-independent iff every server has free_mem >= prompt
+            bool dep = false;
+            for (int q = lane; q < n; q += 32) dep |= v_f[q] < pr;
+            if (__any_sync(FULL, dep)) break;
+          }
+          double best = 0.0;
+          int bi = 0x7fffffff;
+          for (int q = lane; q < n; q += 32) {
+            // sal_load (balancers.py:103-112)
+            double mem = __dmul_rn(beta, (double)((long long)pr - v_f[q]));
+            double que = __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
+            double load = que > mem ? que : mem;
+            if (bi == 0x7fffffff || load < best) { best = load; bi = q; }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            double ob = __shfl_xor_sync(FULL, best, o);
+            int oi = __shfl_xor_sync(FULL, bi, o);
+            if (oi != 0x7fffffff && (bi == 0x7fffffff || ob < best || (ob == best && oi < bi))) { best = ob; bi = oi; }
+          }
+          s = bi;
+          if (lane == 0) {  // note_routed (balancers.py:59-64)
+            v_q[s] += pr;
+            long long f = v_f[s] - pr;
+            v_f[s] = f > 0 ? f : 0;
+            v_if[s] += 1;
+          }
+          __syncwarp();
+        }
+        if (lane == 0) {
+          int* rl = (int*)(scratch + I.scratch_offset + (long long)s * L.total + L.rl);
+          rl[cnt[s]] = k;
+          cnt[s] += 1;
+          rps[s] += pr;
+          rec_srv[k] = s;
+        }
+        __syncwarp();
+        k++;
+        if (!(k < N && __ddiv_rn(arr[k], I.qps_factor) == t)) synced = 0;  // equal times need no sync
+      }
+      if (lane == 0) {
+        S.k = k;
+        S.synced = synced;
+        S.last_poll = last_poll;
+        S.t_lim = k < N ? __ddiv_rn(arr[k], I.qps_factor) : __longlong_as_double(0x7ff0000000000000LL);
+      }
+    }
+    __syncthreads();
+    // ---------------- advance phase: every replica to its boundaries < t_lim ----------------
+    const double t_lim = S.t_lim;
+    for (int s = warp; s < n; s += nwarps) {
+      Eng E;
+      bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap);
+      Srv* sp = (Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
+      E.st = *sp;
+      E.advance(t_lim, cnt[s]);
+      __syncwarp();
+      if (lane == 0) {
+        *sp = E.st;
+        if (E.st.status) atomicExch(&S.err, E.st.status);
+      }
+    }
+    __syncthreads();
+    // ---------------- sync point: fold beta (on_finish, cluster.py:153-154) ----------------
+    if (threadIdx.x == 0) {
+      if (est_beta) {
+        long long c = 0, si = 0, so = 0;
+        for (int s = 0; s < n; ++s) {
+          const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
+          c += sv->fin_cnt; si += sv->fin_in; so += sv->fin_out;
+        }
+        S.beta = c == 0 ? I.beta_prior : __ddiv_rn((double)(si + so), (double)so);  // balancers.py:96-100
+      }
+      S.synced = 1;
+      if (S.k >= N || S.err) S.done = 1;
+    }
+    __syncthreads();
+    if (S.done) break;
+  }
+
+  // ---------------- per-instance stats ----------------
+  if (threadIdx.x == 0) {
+    ssb_stats out;
+    memset(&out, 0, sizeof(out));
+    unsigned long long h = FNV_OFF;
+    int status = S.err;
+    long long evn = 0;
+    for (int s = 0; s < n; ++s) {
+      const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
+      out.iterations += sv->iterations;
+      out.request_steps += sv->rsteps;
+      out.batch_tokens += sv->btokens;
+      out.dispatches += sv->dispatches;
+      out.preempts += sv->preempts;
+      out.parks += sv->parks;
+      out.finished += sv->finished;
+      if (sv->peak > out.peak_batch_tokens) out.peak_batch_tokens = sv->peak;
+      h ^= sv->digest; h *= FNV_PRIME;
+      if (!status && (sv->W != 0 || sv->R != 0)) status = SSB_E_INVARIANT;
+      evn += sv->ev_n;
+    }
+    if (!status && out.finished != N) status = SSB_E_INVARIANT;  // cluster.py:159-161
+    out.digest = h;
+    out.status = status;
+    stats[idx] = out;
+    if (ev_count) ev_count[idx] = evn;
+  }
+}
+
+}  // namespace
+
+// ==========================================================================
+// C ABI
+// ==========================================================================
+static long long header_bytes(int n_inst) { return align_up(64 + 8LL * n_inst, 256); }
+
+extern "C" int32_t ssb_abi_version(void) { return SSB_ABI_VERSION; }
+
+extern "C" const char* ssb_error_string(int32_t code) {
+  switch (code) {
+    case SSB_OK: return "ok";
+    case SSB_E_INFEASIBLE: return "infeasible request";
+    case SSB_E_STALL: return "engine stalled (no schedulable tokens)";
+    case SSB_E_CAPACITY: return "device table capacity exceeded";
+    case SSB_E_INVARIANT: return "invariant violation";
+    case SSB_E_CUDA: return "CUDA error";
+    case SSB_E_ARG: return "bad argument";
+    default: return "unknown";
+  }
+}
+
+extern "C" int32_t ssb_struct_sizes(int64_t* out) {
+  out[0] = sizeof(ssb_engine_params);
+  out[1] = sizeof(ssb_instance);
+  out[2] = sizeof(ssb_stats);
+  out[3] = sizeof(ssb_event);
+  out[4] = sizeof(ssb_summary);
+  out[5] = sizeof(ssb_summary_group);
+  return 6;
+}
+
+extern "C" size_t ssb_prepare(ssb_instance* h, int32_t n_inst) {
+  long long off = header_bytes(n_inst);
+  for (int i = 0; i < n_inst; ++i) {
+    ssb_instance& I = h[i];
+    long long N = I.n_requests;
+    long long Wc = std::max(1LL, N);
+    long long Rc = std::min<long long>(I.engine.pool_blocks, N);
+    if (I.engine.max_running > 0) Rc = std::min<long long>(Rc, I.engine.max_running);
+    Rc = std::max(1LL, Rc);
+    I.wait_cap = (int32_t)Wc;
+    I.run_cap = (int32_t)Rc;
+    I.scratch_offset = off;
+    Layout L = make_layout(Wc, Rc, N, I.n_servers);
+    off += L.total * (long long)std::max(1, I.n_servers);
+  }
+  return (size_t)off;
+}
+
+extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* d_inst, int32_t n_inst,
+                                ssb_trace trace, ssb_records records, ssb_stats* d_stats, void* d_scratch,
+                                size_t scratch_bytes, ssb_event* d_events, int64_t event_cap,
+                                int64_t* d_event_count, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (n_inst <= 0) return SSB_OK;
+  if (!h_inst || !d_inst || !d_stats || !d_scratch) return SSB_E_ARG;
+  long long hb = header_bytes(n_inst);
+  long long need = hb;
+  int max_servers = 1;
+  std::vector<int> singles, multis;
+  for (int i = 0; i < n_inst; ++i) {
+    const ssb_instance& I = h_inst[i];
+    if (I.n_servers < 1 || I.n_requests < 0 || I.n_requests > 0x7fffffffLL || I.wait_cap < 1 || I.run_cap < 1)
+      return SSB_E_ARG;
+    Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers);
+    need = std::max(need, I.scratch_offset + L.total * (long long)I.n_servers);
+    if (I.n_servers == 1) singles.push_back(i); else { multis.push_back(i); max_servers = std::max(max_servers, I.n_servers); }
+  }
+  if ((long long)scratch_bytes < need) return SSB_E_ARG;
+  if (max_servers > 4096) return SSB_E_ARG;
+  std::stable_sort(singles.begin(), singles.end(),
+                   [&](int a, int b) { return h_inst[a].est_cost > h_inst[b].est_cost; });
+  // header: [queue counter][order: singles..., multis...]
+  std::vector<int> hdr(16 + n_inst, 0);
+  for (size_t i = 0; i < singles.size(); ++i) hdr[16 + i] = singles[i];
+  for (size_t i = 0; i < multis.size(); ++i) hdr[16 + singles.size() + i] = multis[i];
+  unsigned char* scratch = (unsigned char*)d_scratch;
+  if (cudaMemcpyAsync(scratch, hdr.data(), sizeof(int) * hdr.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return SSB_E_CUDA;
+  const int* d_order = (const int*)(scratch) + 16;
+  int* d_queue = (int*)scratch;
+  if (!multis.empty()) {
+    int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
+    size_t sm = sizeof(long long) * 4 * max_servers + sizeof(int) * max_servers + 16;
+    k_cluster<<<(unsigned)multis.size(), 32 * nw, sm, stream>>>(d_inst, d_order + singles.size(), trace, records,
+                                                                d_stats, scratch, d_events, event_cap, d_event_count);
+    if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
+  }
+  if (!singles.empty()) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engines, 32 * ENGINE_WARPS_PER_CTA, 0);
+    long long want = ((long long)singles.size() + ENGINE_WARPS_PER_CTA - 1) / ENGINE_WARPS_PER_CTA;
+    int grid = (int)std::min<long long>(want, (long long)sms * std::max(1, occ));
+    k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, 0, stream>>>(d_inst, d_order, (int)singles.size(), d_queue, trace,
+                                                              records, d_stats, scratch, d_events, event_cap,
+                                                              d_event_count);
+    if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
+  }
+  return SSB_OK;
+}

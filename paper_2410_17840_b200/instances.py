@@ -1,0 +1,165 @@
+"""Host-side instance planning: settings + trace -> ssb_instance descriptors.
+
+Restates build_engine (cluster.py:28-47) and the up-front validation of
+run_cluster (cluster.py:74-104) on the host, vectorised over requests, and
+packs the result into the numpy mirror of ``ssb_instance`` (include/ssb.h).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .balancers import BALANCER_NAMES, BetaEstimator, pcg64_words
+from .policies import EngineLimits, make_policy, policy_descriptor
+from .settings import PROFILES, ClusterSettings, EngineSettings, default_params, pool_blocks_for
+from .workload import Trace, as_trace
+
+
+@dataclass
+class ResolvedEngine:
+    """What build_engine() derives from EngineSettings (cluster.py:28-47)."""
+
+    policy: object
+    pool_blocks: int
+    block_size: int
+    cost: object
+    limits: EngineLimits
+
+
+def resolve_engine(es: EngineSettings, policy=None) -> ResolvedEngine:
+    if es.profile not in PROFILES:
+        raise KeyError(es.profile)
+    profile = PROFILES[es.profile]
+    blocks = es.pool_blocks
+    if blocks is None:
+        blocks = pool_blocks_for(es.gpu_mem_bytes, profile, es.block_size)
+    if blocks < 0:
+        raise ValueError(f"total_blocks must be >= 0, got {blocks}")
+    if es.block_size < 1:
+        raise ValueError(f"block_size must be >= 1, got {es.block_size}")
+    cost = default_params(es.profile, es.hardware, **es.cost)
+    if policy is None:
+        policy = make_policy(es.policy, alpha=es.alpha, c=es.c, max_output=es.max_output)
+    limits = EngineLimits(es.max_tokens_per_batch, es.max_running, profile.max_context)
+    return ResolvedEngine(policy, int(blocks), int(es.block_size), cost, limits)
+
+
+def engine_params_record(re: ResolvedEngine) -> np.void:
+    rec = np.zeros((), dtype=_abi.ENGINE_PARAMS)
+    pid, alpha, c, max_output = policy_descriptor(re.policy)
+    rec["policy"] = pid
+    rec["max_output"] = max_output
+    rec["alpha"] = alpha
+    rec["c"] = c
+    rec["block_size"] = re.block_size
+    rec["pool_blocks"] = re.pool_blocks
+    rec["max_tokens_per_batch"] = re.limits.max_tokens_per_batch
+    rec["max_running"] = -1 if re.limits.max_running is None else re.limits.max_running
+    rec["max_context"] = re.limits.max_context
+    rec["mem_base_s"] = re.cost.mem_base_s
+    rec["mem_per_kv_token_s"] = re.cost.mem_per_kv_token_s
+    rec["compute_per_token_s"] = re.cost.compute_per_token_s
+    rec["overhead_s"] = re.cost.overhead_s
+    return rec
+
+
+def check_trace(trace: Trace, re: ResolvedEngine, qps_factor: float = 1.0) -> None:
+    """run_cluster's validation: sorted arrivals then feasibility (cluster.py:80-92)."""
+    arr = trace.arrival if qps_factor == 1.0 else trace.arrival / qps_factor
+    if len(arr) > 1 and np.any(arr[1:] < arr[:-1]):
+        raise ValueError("trace arrivals must be sorted")
+    re.policy.check_feasible_many(trace.prompt, trace.output, re.block_size, re.pool_blocks, re.limits)
+
+
+def instance_record(
+    settings: ClusterSettings,
+    n_requests: int,
+    *,
+    trace_offset: int = 0,
+    record_offset: int = 0,
+    qps_factor: float = 1.0,
+    resolved: ResolvedEngine | None = None,
+) -> np.void:
+    """One ssb_instance for run_cluster(settings, trace) (cluster.py:65-104)."""
+    if settings.n_servers < 1:
+        raise ValueError(f"n_servers must be >= 1, got {settings.n_servers}")
+    bs = settings.balancer
+    if bs.name not in BALANCER_NAMES:
+        raise ValueError(f"unknown balancer {bs.name!r}; expected one of {BALANCER_NAMES}")
+    if bs.poll_interval_s <= 0:
+        raise ValueError(f"poll_interval_s must be > 0, got {bs.poll_interval_s}")  # balancers.py:35-36
+    if bs.name == "sal":
+        BetaEstimator(prior=bs.beta_prior)  # balancers.py:74-75
+    re = resolved or resolve_engine(settings.engine)
+    rec = np.zeros((), dtype=_abi.INSTANCE)
+    rec["engine"] = engine_params_record(re)
+    rec["n_servers"] = settings.n_servers
+    rec["balancer"] = _abi.BALANCER_IDS[bs.name]
+    rec["poll_interval_s"] = float(bs.poll_interval_s)
+    rec["beta_prior"] = float(bs.beta_prior)
+    rec["beta_fixed"] = math.nan if bs.beta_fixed is None else float(bs.beta_fixed)
+    sh, sl, ih, il = pcg64_words(settings.seed)
+    rec["pcg_state_hi"], rec["pcg_state_lo"], rec["pcg_inc_hi"], rec["pcg_inc_lo"] = sh, sl, ih, il
+    rec["qps_factor"] = float(qps_factor)
+    rec["trace_offset"] = trace_offset
+    rec["record_offset"] = record_offset
+    rec["n_requests"] = n_requests
+    return rec
+
+
+@dataclass
+class Batch:
+    """A batch of instances over one concatenated trace."""
+
+    trace: Trace
+    instances: np.ndarray  # INSTANCE records
+    n_records: int
+    labels: list = field(default_factory=list)
+
+
+def make_batch(jobs, *, validate: bool = True) -> Batch:
+    """jobs: iterable of (settings, trace, qps_factor[, label]). Traces that are the
+    same object are stored once and shared by offset (scale_qps is fused into
+    the kernel's trace read)."""
+    traces: list[Trace] = []
+    trace_index: dict[int, int] = {}
+    trace_offs: list[int] = []
+    recs = []
+    labels = []
+    n_trace = 0
+    n_records = 0
+    for job in jobs:
+        settings, trace, factor = job[0], job[1], float(job[2]) if len(job) > 2 else 1.0
+        label = job[3] if len(job) > 3 else None
+        t = as_trace(trace)
+        key = id(trace)
+        if key not in trace_index:
+            trace_index[key] = len(traces)
+            traces.append(t)
+            trace_offs.append(n_trace)
+            n_trace += len(t)
+        toff = trace_offs[trace_index[key]]
+        re = resolve_engine(settings.engine)
+        if validate:
+            check_trace(t, re, factor)
+        recs.append(
+            instance_record(
+                settings, len(t), trace_offset=toff, record_offset=n_records, qps_factor=factor, resolved=re
+            )
+        )
+        labels.append(label)
+        n_records += len(t)
+    if traces:
+        trace_all = Trace(
+            np.concatenate([t.arrival for t in traces]),
+            np.concatenate([t.prompt for t in traces]),
+            np.concatenate([t.output for t in traces]),
+        )
+    else:
+        trace_all = Trace(np.zeros(0), np.zeros(0), np.zeros(0))
+    inst = np.array(recs, dtype=_abi.INSTANCE) if recs else np.zeros(0, dtype=_abi.INSTANCE)
+    return Batch(trace_all, inst, n_records, labels)

@@ -1,0 +1,174 @@
+"""Device driver: marshal a batch of instances to libssb.so and run it on the GPU.
+
+PyTorch provides device memory and the stream; the work is done by the
+sm_100a kernels behind the C ABI (include/ssb.h). There is no CPU fallback:
+without CUDA or without libssb.so every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .instances import Batch
+
+
+class SimulationError(RuntimeError):
+    pass
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise SimulationError("the B200 simulator needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _np_to_dev(torch, arr: np.ndarray, device):
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.to(device, non_blocking=False)
+
+
+def estimate_cost(batch: Batch) -> np.ndarray:
+    """Scheduling hint ~ request-steps: Σ output tokens (+ prompt chunks) per instance."""
+    out = np.zeros(len(batch.instances), dtype=np.int64)
+    csum = np.concatenate([[0], np.cumsum(batch.trace.output.astype(np.int64) + 1)])
+    for i, inst in enumerate(batch.instances):
+        o, n = int(inst["trace_offset"]), int(inst["n_requests"])
+        f = float(inst["engine"]["policy"] == 1) * 4 + 1  # nopreempt steps are slow under backlog
+        out[i] = int((csum[o + n] - csum[o]) * f)
+    return np.clip(out // 16, 0, 2**31 - 1)
+
+
+@dataclass
+class DeviceBatch:
+    """All device buffers of one batch (inputs resident in HBM)."""
+
+    batch: Batch
+    h_inst: np.ndarray
+    d_inst: object
+    d_arrival: object
+    d_prompt: object
+    d_output: object
+    d_ft: object
+    d_fin: object
+    d_fd: object
+    d_pc: object
+    d_srv: object
+    d_stats: object
+    d_scratch: object
+    scratch_bytes: int
+    d_events: object = None
+    d_evcount: object = None
+    event_cap: int = 0
+
+    def trace_c(self) -> _abi.SsbTrace:
+        return _abi.SsbTrace(self.d_arrival.data_ptr(), self.d_prompt.data_ptr(), self.d_output.data_ptr())
+
+    def records_c(self) -> _abi.SsbRecords:
+        return _abi.SsbRecords(self.d_ft.data_ptr(), self.d_fin.data_ptr(), self.d_fd.data_ptr(),
+                               self.d_pc.data_ptr(), self.d_srv.data_ptr())
+
+
+def upload(batch: Batch, *, device=None, events: bool = False, event_cap: int | None = None) -> DeviceBatch:
+    torch = _torch()
+    lib = _abi.load_library()
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    h_inst = np.ascontiguousarray(batch.instances.copy())
+    if len(h_inst):
+        h_inst["est_cost"] = estimate_cost(batch)
+    scratch_bytes = int(lib.ssb_prepare(h_inst.ctypes.data, len(h_inst)))
+    n = batch.n_records
+    db = DeviceBatch(
+        batch=batch,
+        h_inst=h_inst,
+        d_inst=_np_to_dev(torch, h_inst.view(np.uint8), device),
+        d_arrival=_np_to_dev(torch, batch.trace.arrival, device),
+        d_prompt=_np_to_dev(torch, batch.trace.prompt, device),
+        d_output=_np_to_dev(torch, batch.trace.output, device),
+        d_ft=torch.empty(n, dtype=torch.float64, device=device),
+        d_fin=torch.empty(n, dtype=torch.float64, device=device),
+        d_fd=torch.empty(n, dtype=torch.float64, device=device),
+        d_pc=torch.empty(n, dtype=torch.int32, device=device),
+        d_srv=torch.empty(n, dtype=torch.int32, device=device),
+        d_stats=torch.zeros(len(h_inst) * _abi.STATS.itemsize, dtype=torch.uint8, device=device),
+        d_scratch=torch.empty(max(scratch_bytes, 256), dtype=torch.uint8, device=device),
+        scratch_bytes=scratch_bytes,
+    )
+    if events:
+        cap = event_cap or int(max(1, max((int(i["n_requests"]) for i in h_inst), default=1)) * 12 + 64)
+        cap = cap * int(max((int(i["n_servers"]) for i in h_inst), default=1))
+        db.event_cap = cap
+        db.d_events = torch.empty(len(h_inst) * cap * _abi.EVENT.itemsize, dtype=torch.uint8, device=device)
+        db.d_evcount = torch.zeros(len(h_inst), dtype=torch.int64, device=device)
+    return db
+
+
+def launch(db: DeviceBatch, stream=None) -> None:
+    """Enqueue the simulation kernels on `stream` (default: torch's current stream)."""
+    torch = _torch()
+    lib = _abi.load_library()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    rc = lib.ssb_simulate(
+        db.h_inst.ctypes.data, db.d_inst.data_ptr(), len(db.h_inst), db.trace_c(), db.records_c(),
+        db.d_stats.data_ptr(), db.d_scratch.data_ptr(), db.scratch_bytes,
+        db.d_events.data_ptr() if db.d_events is not None else None, db.event_cap,
+        db.d_evcount.data_ptr() if db.d_evcount is not None else None, ctypes.c_void_p(stream.cuda_stream),
+    )
+    if rc != 0:
+        raise SimulationError(f"ssb_simulate: {lib.ssb_error_string(rc).decode()} ({rc})")
+
+
+class HostResults:
+    def __init__(self, n):
+        self.first_token = np.empty(n)
+        self.finish = np.empty(n)
+        self.first_dispatch = np.empty(n)
+        self.preempt_count = np.empty(n, dtype=np.int32)
+        self.server = np.empty(n, dtype=np.int32)
+
+
+def download(db: DeviceBatch):
+    """Device -> host: (records, stats[, events per instance])."""
+    rec = HostResults(db.batch.n_records)
+    rec.first_token = db.d_ft.cpu().numpy()
+    rec.finish = db.d_fin.cpu().numpy()
+    rec.first_dispatch = db.d_fd.cpu().numpy()
+    rec.preempt_count = db.d_pc.cpu().numpy()
+    rec.server = db.d_srv.cpu().numpy()
+    stats = db.d_stats.cpu().numpy().view(_abi.STATS).copy()
+    if db.d_events is None:
+        return rec, stats
+    ev = db.d_events.cpu().numpy().view(_abi.EVENT).reshape(len(db.h_inst), db.event_cap)
+    per = []
+    for i, inst in enumerate(db.h_inst):
+        ns = int(inst["n_servers"])
+        sl = db.event_cap // ns
+        lists = []
+        for s in range(ns):
+            seg = ev[i, s * sl:(s + 1) * sl]
+            valid = seg[seg["code"] >= 0]
+            lists.append(valid.copy())
+        per.append(lists)
+    return rec, stats, per
+
+
+def run_batch(batch: Batch, *, events: bool = False, event_cap: int | None = None, check: bool = False):
+    """Upload, simulate, download. Returns (records, stats[, events])."""
+    torch = _torch()
+    db = upload(batch, events=events, event_cap=event_cap)
+    launch(db)
+    torch.cuda.synchronize()
+    out = download(db)
+    if check:
+        bad = np.flatnonzero(out[1]["status"] != 0)
+        if len(bad):
+            lib = _abi.load_library()
+            code = int(out[1]["status"][bad[0]])
+            raise SimulationError(f"instance {int(bad[0])}: {lib.ssb_error_string(code).decode()} ({code})")
+    return out

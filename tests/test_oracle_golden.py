@@ -1,0 +1,67 @@
+"""Pin the CPU oracle (oracle/ssb_oracle.c) against fixtures produced by the
+Python reference itself (tests/golden/make_golden.py). CPU only."""
+
+import numpy as np
+import pytest
+
+import scenarios as S
+from helpers import compare_instance, load_golden, scenario_batch
+from oracle import oracle as O
+
+GROUPS_FAST = ["engine_unit", "cluster_unit", "c2", "c3", "fuzz_engine", "fuzz_cluster", "c6"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build_oracle():
+    O.build()
+
+
+@pytest.mark.parametrize("group", GROUPS_FAST)
+def test_oracle_matches_reference(group):
+    golden = load_golden(group)
+    scs = S.GROUPS[group]()
+    batch = scenario_batch(scs)
+    rec, stats = O.run_batch(batch, mode=0, threads=4)
+    failures = {}
+    for i, sc in enumerate(scs):
+        bad = compare_instance(sc, golden, batch, i, rec, stats)
+        if bad:
+            failures[sc["name"]] = bad
+    assert not failures, dict(list(failures.items())[:5])
+
+
+def test_oracle_engine_run_equals_run_cluster():
+    """Engine.run (engine.py:236) == run_cluster with one server (tests/test_cluster.py:39-60)."""
+    scs = [s for s in S.engine_unit_scenarios() + S.fuzz_engine_scenarios()]
+    batch = scenario_batch(scs)
+    r0, s0 = O.run_batch(batch, mode=0)
+    r1, s1 = O.run_batch(batch, mode=1)
+    assert np.array_equal(s0, s1)
+    assert np.array_equal(r0.first_token, r1.first_token) and np.array_equal(r0.finish, r1.finish)
+
+
+def test_oracle_event_streams_match_reference():
+    """Full (event, time, id) streams, like criterion 6 (test_acceptance.py:314-317)."""
+    golden = load_golden("engine_unit")
+    scs = S.engine_unit_scenarios()
+    batch = scenario_batch(scs)
+    _, _, evs = O.run_batch(batch, events=True)
+    for sc, ev in zip(scs, evs):
+        want = [tuple(e) for e in golden[sc["name"]]["events"][0]]
+        got = [(int(e["code"]), int(e["request_id"]), float(e["time"])) for e in ev]
+        assert got == want, sc["name"]
+
+
+def test_oracle_summary_matches_reference():
+    golden = load_golden("cluster_unit")
+    scs = S.cluster_unit_scenarios()
+    batch = scenario_batch(scs)
+    rec, stats = O.run_batch(batch)
+    for i, sc in enumerate(scs):
+        inst = batch.instances[i]
+        n, o, to = int(inst["n_requests"]), int(inst["record_offset"]), int(inst["trace_offset"])
+        s = O.summarize(batch.trace.arrival[to:to + n] / inst["qps_factor"], batch.trace.prompt[to:to + n],
+                        batch.trace.output[to:to + n], rec.first_token[o:o + n], rec.finish[o:o + n],
+                        rec.preempt_count[o:o + n])
+        for k, v in golden[sc["name"]]["summary"].items():
+            assert s[k] == v, (sc["name"], k)
