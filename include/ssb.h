@@ -91,8 +91,15 @@ typedef struct {
   int32_t wait_cap;             /* waiting-ring capacity per server                 */
   int32_t run_cap;              /* running-table capacity per server                */
   int32_t est_cost;             /* scheduling hint (larger = start earlier)         */
-  int32_t _pad1;
+  int32_t flags;                /* SSB_FLAG_*                                       */
 } ssb_instance;
+
+/* Running tables live in shared memory with SSB_SMEM_RUN_CAP entries per
+ * engine unless SSB_FLAG_GLOBAL_TABLES is set (then global, sized run_cap).
+ * An instance that outgrows the shared table ends with SSB_E_CAPACITY and is
+ * simply re-run with the flag (the host shim does this automatically). */
+#define SSB_SMEM_RUN_CAP 256
+#define SSB_FLAG_GLOBAL_TABLES 1
 
 /* Trace SoA, TraceEntry (workload.py:42-56); arrivals sorted per instance. */
 typedef struct {

@@ -18,6 +18,7 @@ POLICY_IDS = {"fcfs": 0, "nopreempt": 1, "trail_plus": 2, "larry": 3}
 BALANCER_IDS = {"rr": 0, "random": 1, "p2c": 2, "sal": 3}
 EVENT_NAMES = ("enqueue", "dispatch", "preempt", "park", "first_token", "finish")
 
+SSB_FLAG_GLOBAL_TABLES = 1
 SSB_OK, SSB_E_INFEASIBLE, SSB_E_STALL, SSB_E_CAPACITY, SSB_E_INVARIANT, SSB_E_CUDA, SSB_E_ARG = range(7)
 
 ENGINE_PARAMS = np.dtype(
@@ -60,7 +61,7 @@ INSTANCE = np.dtype(
         ("wait_cap", "<i4"),
         ("run_cap", "<i4"),
         ("est_cost", "<i4"),
-        ("_pad1", "<i4"),
+        ("flags", "<i4"),
     ],
     align=True,
 )

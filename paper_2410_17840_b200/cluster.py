@@ -1,0 +1,200 @@
+"""Drop-in simulation entry points (cluster.py / engine.py of the reference).
+
+* ``run_cluster(settings, trace, *, engines=None) -> list[MetricsRecord]``
+  — cluster.py:65-174, same signature, validation, errors and results
+  (bit-exact), computed by the sm_100a kernels.
+* ``build_engine(settings) -> Engine`` and ``Engine(...).run(trace)``
+  — cluster.py:28-47 / engine.py:236-265.
+* ``simulate_jobs(jobs)`` — the batched form: many independent
+  (settings, trace, qps_factor) instances in one device launch, records as
+  structure-of-arrays, optional device summaries. This is what makes a sweep
+  (capacity_sweep, BASELINE config 4) a single launch.
+
+Errors mirror the reference: ValueError for unsorted traces / bad settings,
+InfeasibleRequestError (policies.py:18) before simulating, StallError
+(engine.py:138) and RuntimeError from the device status codes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from . import instances as I
+from .metrics import MetricsRecord, RecordsSoA, Summary, SummaryExtras, summary_groups, summarize_device, _summary_from_row
+from .policies import EngineLimits
+from .settings import ClusterSettings, CostParams, EngineSettings, KvBlockPool
+from .workload import Trace, as_trace
+
+
+class StallError(RuntimeError):
+    """The engine has work but cannot schedule a single token (engine.py:138-139)."""
+
+
+def _raise_status(code: int, where: str) -> None:
+    if code == _abi.SSB_OK:
+        return
+    lib = _abi.load_library()
+    msg = f"{where}: {lib.ssb_error_string(code).decode()}"
+    if code == _abi.SSB_E_STALL:
+        raise StallError(msg)
+    if code == _abi.SSB_E_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+class Engine:
+    """Engine descriptor (engine.py:142-169). ``run`` simulates a whole trace on
+    the device; afterwards ``iterations``, ``peak_batch_tokens``,
+    ``request_steps``, ``batch_tokens`` and (if ``record_events``)
+    ``event_log`` describe what happened, like the reference's attributes."""
+
+    def __init__(self, pool, policy, cost: CostParams, *, block_size: int = 16,
+                 max_tokens_per_batch: int = 1024, max_running: int | None = None, max_context: int = 8192,
+                 record_events: bool = False):
+        if isinstance(pool, KvBlockPool):  # Engine(KvBlockPool(blocks, bs), policy, cost, ...) as in the reference
+            pool_blocks, block_size = pool.total_blocks, pool.block_size
+            self.pool = pool
+        else:
+            pool_blocks = int(pool)
+            self.pool = KvBlockPool(pool_blocks, block_size)
+        self.resolved = I.ResolvedEngine(policy=policy, pool_blocks=int(pool_blocks), block_size=int(block_size),
+                                         cost=cost, limits=EngineLimits(max_tokens_per_batch, max_running,
+                                                                        max_context))
+        self.record_events = record_events
+        self.policy = policy
+        self.limits = self.resolved.limits
+        self._used = False
+        self.iterations = 0
+        self.peak_batch_tokens = 0
+        self.request_steps = 0
+        self.batch_tokens = 0
+        self.event_log: list[tuple[str, float, int, str]] = []
+
+    def run(self, trace, validate: bool = True) -> list[MetricsRecord]:
+        """engine.py:236-265 (a fresh engine is required)."""
+        if self._used:
+            raise RuntimeError("run() needs a fresh engine")
+        settings = ClusterSettings(n_servers=1, engine=EngineSettings(max_tokens_per_batch=self.limits.max_tokens_per_batch))
+        settings.balancer.name = "rr"
+        return run_cluster(settings, trace, engines=[self], _validate=validate)
+
+    def event_lines(self) -> list[str]:
+        return [f"{ev},{t!r},{rid},{d}" for ev, t, rid, d in self.event_log]
+
+
+def build_engine(settings: EngineSettings, *, record_events: bool = False) -> Engine:
+    """cluster.py:28-47."""
+    re = I.resolve_engine(settings)
+    return Engine(re.pool_blocks, re.policy, re.cost, block_size=re.block_size,
+                  max_tokens_per_batch=re.limits.max_tokens_per_batch, max_running=re.limits.max_running,
+                  max_context=re.limits.max_context, record_events=record_events)
+
+
+@dataclass
+class JobResult:
+    """One instance's outcome."""
+
+    label: object
+    records: RecordsSoA
+    stats: np.void
+    summary: Summary | None = None
+    extras: SummaryExtras | None = None
+    events: list = field(default_factory=list)
+
+
+def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, validate: bool = True,
+                  resolved=None) -> list[JobResult]:
+    """Simulate independent instances in one launch. jobs: (settings, trace[, qps_factor[, label]])."""
+    import torch
+
+    from . import simulate
+
+    jobs = list(jobs)
+    if resolved is None:
+        batch = I.make_batch(jobs, validate=validate)
+    else:  # explicit ResolvedEngine per job (prebuilt engines)
+        recs, traces, n_rec = [], [], 0
+        for (job, re) in zip(jobs, resolved):
+            t = as_trace(job[1])
+            f = float(job[2]) if len(job) > 2 else 1.0
+            if validate:
+                I.check_trace(t, re, f)
+            recs.append(I.instance_record(job[0], len(t), trace_offset=n_rec, record_offset=n_rec, qps_factor=f,
+                                          resolved=re))
+            traces.append(t)
+            n_rec += len(t)
+        tr = Trace(np.concatenate([t.arrival for t in traces]), np.concatenate([t.prompt for t in traces]),
+                   np.concatenate([t.output for t in traces]))
+        batch = I.Batch(tr, np.array(recs, dtype=_abi.INSTANCE), n_rec, [j[3] if len(j) > 3 else None for j in jobs])
+    db = simulate.upload(batch, events=events)
+    simulate.launch(db)
+    torch.cuda.synchronize()
+    if simulate.retry_overflows(db):
+        if events:
+            simulate.launch(db)
+        torch.cuda.synchronize()
+    srows = None
+    if summaries:
+        inst = db.h_inst
+        groups = summary_groups([(int(i["record_offset"]), int(i["n_requests"])) for i in inst],
+                                trace_offsets=[int(i["trace_offset"]) for i in inst],
+                                qps=[float(i["qps_factor"]) for i in inst])
+        ok = np.array([int(i["n_requests"]) > 0 for i in inst])
+        srows = np.zeros(len(inst), dtype=_abi.SUMMARY)
+        if ok.any():
+            srows[ok] = summarize_device(db.trace_c(), db.records_c(), groups[ok])
+    out = simulate.download(db)
+    rec, stats = out[0], out[1]
+    results = []
+    for i, inst in enumerate(db.h_inst):
+        n, o, to = int(inst["n_requests"]), int(inst["record_offset"]), int(inst["trace_offset"])
+        arr = batch.trace.arrival[to:to + n]
+        f = float(inst["qps_factor"])
+        if f != 1.0:
+            arr = arr / f
+        soa = RecordsSoA(arr, batch.trace.prompt[to:to + n], batch.trace.output[to:to + n],
+                         rec.first_token[o:o + n], rec.finish[o:o + n], rec.preempt_count[o:o + n],
+                         rec.server[o:o + n], rec.first_dispatch[o:o + n])
+        r = JobResult(batch.labels[i] if i < len(batch.labels) else None, soa, stats[i])
+        if srows is not None and n > 0:
+            r.summary, r.extras = _summary_from_row(srows[i])
+        if events:
+            r.events = out[2][i]
+        results.append(r)
+    return results
+
+
+def run_cluster(settings: ClusterSettings, trace, *, engines: list[Engine] | None = None,
+                _validate: bool = True) -> list[MetricsRecord]:
+    """cluster.py:65-174: one record per request, in request-id order."""
+    n = settings.n_servers
+    if engines is not None and len(engines) != n:
+        raise ValueError(f"expected {n} engines, got {len(engines)}")
+    resolved = None
+    if engines is not None:
+        r0 = engines[0].resolved
+        for e in engines[1:]:
+            if e.resolved != r0:
+                raise NotImplementedError("heterogeneous engines in one cluster are not supported on the device")
+        for e in engines:
+            if e._used:
+                raise RuntimeError("run() needs a fresh engine")
+        resolved = [r0]
+    t = as_trace(trace)
+    rec_events = bool(engines) and any(e.record_events for e in engines)
+    res = simulate_jobs([(settings, t, 1.0)], events=rec_events, validate=_validate, resolved=resolved)[0]
+    _raise_status(int(res.stats["status"]), "run_cluster")
+    if engines is not None:
+        for s, e in enumerate(engines):
+            e._used = True
+            e.iterations = int(res.stats["iterations"]) if n == 1 else e.iterations
+            e.peak_batch_tokens = int(res.stats["peak_batch_tokens"])
+            e.request_steps = int(res.stats["request_steps"]) if n == 1 else e.request_steps
+            e.batch_tokens = int(res.stats["batch_tokens"]) if n == 1 else e.batch_tokens
+            if rec_events:
+                e.event_log = [(_abi.EVENT_NAMES[int(x["code"])], float(x["time"]), int(x["request_id"]), "")
+                               for x in res.events[s]]
+    return res.records.to_records()

@@ -109,6 +109,27 @@ __device__ __forceinline__ int warp_sum(int v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
+// single-instruction (REDUX) warp sum for per-chunk values that fit in 32 bits
+__device__ __forceinline__ int redux_add(int v) { return (int)__reduce_add_sync(FULL, (unsigned)v); }
+
+// total order on binary64 as unsigned 64-bit keys (larger double -> larger key)
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  long long b = __double_as_longlong(x);
+  return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ULL);
+}
+// lanes (mask) holding the maximum 64-bit key among lanes with `has` (0 if none): two REDUX.MAX
+__device__ __forceinline__ unsigned warp_argmax_u64(unsigned long long key, bool has) {
+  if (!__any_sync(FULL, has)) return 0u;
+  unsigned hi = has ? (unsigned)(key >> 32) : 0u;
+  unsigned m1 = __reduce_max_sync(FULL, hi);
+  bool c1 = has && hi == m1;
+  unsigned lo = c1 ? (unsigned)key : 0u;
+  unsigned m2 = __reduce_max_sync(FULL, lo);
+  return __ballot_sync(FULL, c1 && lo == m2);
+}
+__device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool has) {
+  return warp_argmax_u64(~key, has);
+}
 
 struct Eng {
   Cfg cfg;
@@ -291,6 +312,12 @@ struct Eng {
   __device__ int select_prefix() {
     long long slots = cfg.max_running < 0 ? (1LL << 40) : (long long)cfg.max_running - st.R;  // policies.py:70-73
     int limit = (cfg.policy == SSB_POLICY_FCFS) ? st.free_blocks : cfg.pool - st.committed;
+    if (st.W == 0 || slots <= 0) return 0;
+    {  // head-of-line check first (uniform load): the common backlogged case dispatches nothing
+      int pos = phys(0);
+      int need0 = (cfg.policy == SSB_POLICY_FCFS) ? blocks(p.w_pend[pos]) : p.w_key[pos];
+      if (need0 > limit) return 0;
+    }
     int D = 0, used = 0;
     for (int base = 0; base < st.W; base += 32) {
       int k = base + lane;
@@ -345,17 +372,17 @@ struct Eng {
         bool better = !found || (sc > b_sc) || (sc == b_sc && (enq < b_enq || (enq == b_enq && rid < b_rid)));
         if (better) { found = true; b_sc = sc; b_enq = enq; b_rid = rid; b_k = k; }
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        int of = __shfl_xor_sync(FULL, (int)found, o);
-        double osc = __shfl_xor_sync(FULL, b_sc, o);
-        double oenq = __shfl_xor_sync(FULL, b_enq, o);
-        int orid = __shfl_xor_sync(FULL, b_rid, o);
-        int ok_ = __shfl_xor_sync(FULL, b_k, o);
-        bool take = of && (!found || (osc > b_sc) ||
-                           (osc == b_sc && (oenq < b_enq || (oenq == b_enq && orid < b_rid))));
-        if (take) { found = true; b_sc = osc; b_enq = oenq; b_rid = orid; b_k = ok_; }
-      }
+      // warp argmax of (score, -enqueue_time, -id): REDUX on orderable keys, ties rare
+      unsigned win = warp_argmax_u64(dkey(b_sc), found);
+      if (win == 0u) break;
+      if (win & (win - 1)) win = warp_argmax_u64(~dkey(b_enq), found && ((win >> lane) & 1u));
+      if (win & (win - 1)) win = warp_argmax_u64(~(unsigned long long)(unsigned)b_rid, found && ((win >> lane) & 1u));
+      const int wl = __ffs(win) - 1;
+      b_sc = __shfl_sync(FULL, b_sc, wl);
+      b_enq = __shfl_sync(FULL, b_enq, wl);
+      b_rid = __shfl_sync(FULL, b_rid, wl);
+      b_k = __shfl_sync(FULL, b_k, wl);
+      found = true;
       if (!found) break;
       int pos = phys(b_k);
       int pend = p.w_pend[pos];
@@ -461,13 +488,10 @@ struct Eng {
         }
         if (ok) { best = key; best_k = k; }
       }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        unsigned long long ob = __shfl_xor_sync(FULL, best, o);
-        int ok_ = __shfl_xor_sync(FULL, best_k, o);
-        if (ob < best) { best = ob; best_k = ok_; }
-      }
-      if (best == ~0ULL) break;
+      unsigned win = warp_argmin_u64(best, best != ~0ULL);  // keys are unique
+      if (win == 0u) break;
+      best = __shfl_sync(FULL, best, __ffs(win) - 1);
+      best_k = __shfl_sync(FULL, best_k, __ffs(win) - 1);
       int pos = phys(best_k);
       int need = blocks(p.w_pend[pos]);
       int rem = (int)(best >> 32);
@@ -578,7 +602,7 @@ struct Eng {
     }
     need_sum = warp_sum(need_sum);
     pend_sum = warp_sum_ll(pend_sum);
-    res_sum = warp_sum(res_sum);
+    res_sum = warp_sum(res_sum);  // (several chunks: per-lane partial sums may exceed 32-bit REDUX range)
     st.free_blocks -= need_sum;  // try_allocate (kvmem.py:106-117)
     if (st.free_blocks < 0) st.status = SSB_E_INVARIANT;  // "policy over-admitted" (engine.py:288-292)
     st.committed += res_sum;
@@ -625,12 +649,11 @@ struct Eng {
       unsigned mp = __ballot_sync(FULL, in_pf);
       if (in_pf) p.l_b[npf_ + __popc(mp & lanemask_lt())] = j;
       npf_ += __popc(mp);
-      long long ctx = in_dec ? (long long)(pr + g) : (in_pf ? (long long)f : 0);
-      res += ctx;
+      int ctx = in_dec ? pr + g : (in_pf ? f : 0);
+      res += redux_add(ctx);
       dec_seen += __popc(md);
       pf_used = __shfl_sync(FULL, incl, 31);
     }
-    res = warp_sum_ll(res);
     int pf_tokens = (int)min((long long)budget, (long long)pf_used);
     total = n_dec_plan + pf_tokens;
     resident = res;
@@ -681,10 +704,15 @@ struct Eng {
         }
       }
       int d = act ? rel - extra : 0;
-      int excl = warp_incl_scan(d, lane) - d;
-      bool fail = act && grow && extra > st.free_blocks + excl;
-      unsigned mf = __ballot_sync(FULL, fail);
-      int fl = mf ? __ffs(mf) - 1 : 32;
+      int excl = 0, fl = 32;
+      // grows only consume and finishes only release: if the chunk's total
+      // demand fits the free pool no grow can fail, whatever the order
+      if (redux_add(extra) > st.free_blocks) {
+        excl = warp_incl_scan(d, lane) - d;
+        bool fail = act && grow && extra > st.free_blocks + excl;
+        unsigned mf = __ballot_sync(FULL, fail);
+        fl = mf ? __ffs(mf) - 1 : 32;
+      }
       bool commit = act && lane < fl;
       // commit lanes [start, fl)
       unsigned m_first = __ballot_sync(FULL, commit && first);
@@ -704,12 +732,11 @@ struct Eng {
         }
         if (fin) rec_fin[rid] = st.clock;
       }
-      int dsum = __shfl_sync(FULL, excl + d, 31);  // total over all lanes...
-      // ...but only lanes < fl commit: take the exclusive prefix at fl
-      int dcommit = (fl == 32) ? dsum : __shfl_sync(FULL, excl, fl & 31);
+      // released-minus-grown blocks of the committed lanes
+      int dcommit = (fl == 32) ? redux_add(d) : __shfl_sync(FULL, excl, fl & 31);
       st.free_blocks += dcommit;
       if (PREFILL) {
-        int chunk_sum = warp_sum(commit ? plan - 1 : 0);
+        int chunk_sum = redux_add(commit ? plan - 1 : 0);
         st.pf_pend -= chunk_sum;
         if (PREFILL) emit2(m_first, SSB_EV_FIRST_TOKEN, m_fin, SSB_EV_FINISH, rid);
       } else {
@@ -721,10 +748,10 @@ struct Eng {
         removed_any = true;
         st.finished += n_fin;
         st.fin_cnt += n_fin;
-        st.fin_in += warp_sum(commit && fin ? pr : 0);
-        st.fin_out += warp_sum(commit && fin ? out : 0);
+        st.fin_in += redux_add(commit && fin ? pr : 0);
+        st.fin_out += redux_add(commit && fin ? out : 0);
         if (cfg.policy == SSB_POLICY_NOPREEMPT)
-          st.committed -= warp_sum(commit && fin ? wkey_for(pr, out, 0) : 0);
+          st.committed -= redux_add(commit && fin ? wkey_for(pr, out, 0) : 0);
       }
       __syncwarp();
       if (fl == 32) break;
@@ -795,6 +822,103 @@ struct Eng {
     return removed;
   }
 
+  // ---- fused _form_batch + latency + _apply_progress for R <= 32 ----
+  // The whole running table is one chunk held in registers: the plan, the
+  // resident-KV and token sums (REDUX), the clock update and the progress
+  // commit need no memory round trip in between. When the plan's total grow
+  // demand exceeds the free pool (rare: memory pressure) it hands over to the
+  // general ordered path (progress_group) with the plan written to memory.
+  __device__ void batch_progress_small() {
+    const int cap = cfg.cap;
+    const bool valid = lane < st.R;
+    int s = ST_GONE, pr = 0, out = 0, g = 0, f = 0, rid = 0;
+    if (valid) { s = p.r_st[lane]; pr = p.r_prompt[lane]; out = p.r_out[lane]; g = p.r_gen[lane]; f = p.r_pfd[lane]; rid = p.r_rid[lane]; }
+    const unsigned lt = lanemask_lt();
+    const bool dec = s == ST_DECODE, pf = s == ST_PREFILL;
+    const unsigned md = __ballot_sync(FULL, dec);
+    const bool in_dec = dec && __popc(md & lt) < cap;  // decodes first, 1 token each (engine.py:303-309)
+    const int n_dec_plan = min(__popc(md), cap);
+    const int B = cap - n_dec_plan;
+    const unsigned mpf = __ballot_sync(FULL, pf);
+    const int pend = pf ? pr + g - f : 0;
+    int before = 0;
+    if (mpf & (mpf - 1)) before = warp_incl_scan(pend, lane) - pend;  // >1 prefilling: claimed earlier
+    const int chunk = (pf && B - before > 0) ? min(pend, B - before) : 0;  // engine.py:311-318
+    const bool in_pf = chunk > 0;
+    const unsigned m_pf = __ballot_sync(FULL, in_pf);
+    const unsigned m_dec = __ballot_sync(FULL, in_dec);
+    const int resident = redux_add(in_dec ? pr + g : (in_pf ? f : 0));  // engine.py:217-218
+    const int pf_tokens = redux_add(chunk);
+    const int total = n_dec_plan + pf_tokens;
+    if (total == 0) { st.status = SSB_E_STALL; return; }  // engine.py:209-214
+    st.rsteps += __popc(m_dec) + __popc(m_pf);
+    st.btokens += total;
+    {  // iteration_latency (costmodel.py:45-47); clock += latency (engine.py:219-220)
+      double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, (double)resident));
+      double comp = __dmul_rn(cfg.compute, (double)total);
+      st.clock = __dadd_rn(st.clock, __dadd_rn(cfg.overhead, comp > mem ? comp : mem));
+    }
+    // progress: prefill chunks land, first tokens, decode tokens (engine.py:328-357)
+    const int f2 = f + chunk;
+    const bool complete = in_pf && f2 >= pr + g;
+    const bool first = complete && g == 0;
+    const bool recompute = complete && g > 0;
+    int extra = 0;
+    if (first) extra = blocks(pr + 1) - blocks(pr);
+    else if (in_dec) extra = blocks(pr + g + 1) - blocks(pr + g);
+    const int need = redux_add(extra);
+    if (need > st.free_blocks) {
+      // memory pressure: ordered grows with eviction (general path)
+      if (valid) p.r_plan[lane] = in_dec ? 1 : (in_pf ? chunk + 1 : 0);
+      if (in_pf) p.l_b[__popc(m_pf & lt)] = lane;
+      __syncwarp();
+      bool removed = progress(__popc(m_pf));
+      if (removed) compact_running();
+      if (total > st.peak) st.peak = total;
+      st.iterations += 1;
+      return;
+    }
+    const bool fin = (first && out == 1) || (in_dec && g + 1 == out);
+    const int rel = fin ? (first ? blocks(pr + 1) : blocks(pr + g + 1)) : 0;
+    st.free_blocks += redux_add(rel) - need;
+    int g2 = first ? 1 : (in_dec ? g + 1 : g);
+    int s2 = fin ? ST_GONE : ((first || recompute) ? ST_DECODE : s);
+    if (first) rec_ft[rid] = st.clock;
+    if (fin) rec_fin[rid] = st.clock;
+    const unsigned m_first = __ballot_sync(FULL, first);
+    const unsigned m_fin = __ballot_sync(FULL, fin);
+    const unsigned m_rec = __ballot_sync(FULL, recompute);
+    if (m_first | m_fin) {
+      emit2(m_first, SSB_EV_FIRST_TOKEN, m_fin & m_pf, SSB_EV_FINISH, rid);  // prefill section first
+      emit(m_fin & m_dec, SSB_EV_FINISH, rid);                             // then decodes
+    }
+    st.pf_pend -= pf_tokens;
+    st.ndec += __popc(m_first | m_rec) - __popc(m_fin);
+    if (m_fin) {
+      const int nf = __popc(m_fin);
+      st.finished += nf;
+      st.fin_cnt += nf;
+      st.fin_in += redux_add(fin ? pr : 0);
+      st.fin_out += redux_add(fin ? out : 0);
+      if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= redux_add(fin ? wkey_for(pr, out, 0) : 0);
+      // compact in registers: kept entries move down to their rank
+      const bool keep = valid && s2 != ST_GONE;
+      const unsigned mk = __ballot_sync(FULL, keep);
+      __syncwarp();
+      if (keep) {
+        const int d = __popc(mk & lt);
+        p.r_rid[d] = rid; p.r_prompt[d] = pr; p.r_out[d] = out; p.r_gen[d] = g2; p.r_pfd[d] = f2; p.r_st[d] = s2;
+      }
+      st.R = __popc(mk);
+    } else {
+      if (in_pf) { p.r_pfd[lane] = f2; p.r_gen[lane] = g2; p.r_st[lane] = s2; }
+      else if (in_dec) p.r_gen[lane] = g2;
+    }
+    __syncwarp();
+    if (total > st.peak) st.peak = total;
+    st.iterations += 1;
+  }
+
   // ---- Engine.step (engine.py:193-234) ----
   __device__ void step() {
     if (!has_work()) { st.status = SSB_E_STALL; return; }
@@ -818,6 +942,7 @@ struct Eng {
     }
     apply_dispatches(nd, prefix);  // then dispatches (engine.py:205-206)
     if (st.status) return;
+    if (st.R <= 32) { batch_progress_small(); return; }
     int total, nent, npf;
     long long resident;
     form_batch(total, resident, nent, npf);
@@ -836,21 +961,29 @@ struct Eng {
   }
 
   // ---- advance: process every boundary with time < t_lim (cluster.py:142-157 / engine.py:256-265) ----
+  __device__ __forceinline__ double next_arrival(int n_avail) const {
+    if (st.next_arr >= n_avail) return __longlong_as_double(0x7ff0000000000000LL);  // +inf: none routed yet
+    int rid = (cfg.n_servers == 1) ? st.next_arr : p.rl[st.next_arr];
+    return arrival_of(rid);
+  }
   __device__ void advance(double t_lim, int n_avail) {
+    double next_t = next_arrival(n_avail);
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
     while (st.status == SSB_OK) {
       double nb;
       if (!has_work()) {
-        if (st.next_arr >= n_avail) break;  // idle until the next routed arrival
-        int rid = (cfg.n_servers == 1) ? st.next_arr : p.rl[st.next_arr];
-        double a = arrival_of(rid);
-        nb = a > st.clock ? a : st.clock;  // wake = max(t, clock) (cluster.py:139)
+        if (next_t == INF) break;            // idle until the next routed arrival
+        nb = next_t > st.clock ? next_t : st.clock;  // wake = max(t, clock) (cluster.py:139)
       } else {
         nb = st.clock;
       }
       if (!(nb < t_lim)) break;  // ties: arrivals before boundaries (cluster.py:62)
       st.clock = nb;             // advance_to (engine.py:186-191)
-      enqueue_ready(n_avail);
-      if (st.status) break;
+      if (next_t <= st.clock) {
+        enqueue_ready(n_avail);
+        if (st.status) break;
+        next_t = next_arrival(n_avail);
+      }
       step();
     }
   }

@@ -109,10 +109,28 @@ __device__ inline void init_srv(Srv& s, const Cfg& c) {
   s.R = s.W = s.whead = s.committed = s.next_arr = s.status = s.ndec = 0;
 }
 
+constexpr int SM_COLS = 9;  // r_rid r_prompt r_out r_gen r_pfd r_st r_plan l_a l_b
+constexpr int RS = SSB_SMEM_RUN_CAP;
+
+// sm_tab: this engine's shared-memory running table (SM_COLS x RS ints) or
+// nullptr for the global layout (SSB_FLAG_GLOBAL_TABLES).
 __device__ inline void bind_engine(Eng& E, const ssb_instance& I, const Cfg& cfg, unsigned char* scratch, int server,
-                                   const Layout& L, ssb_trace tr, ssb_records rec, ssb_event* ev, long long ev_cap) {
+                                   const Layout& L, ssb_trace tr, ssb_records rec, ssb_event* ev, long long ev_cap,
+                                   int* sm_tab = nullptr) {
   E.cfg = cfg;
   E.p = make_ptrs(scratch + I.scratch_offset + (long long)server * L.total, L);
+  if (sm_tab != nullptr && !(I.flags & SSB_FLAG_GLOBAL_TABLES)) {
+    E.p.r_rid = sm_tab;
+    E.p.r_prompt = sm_tab + RS;
+    E.p.r_out = sm_tab + 2 * RS;
+    E.p.r_gen = sm_tab + 3 * RS;
+    E.p.r_pfd = sm_tab + 4 * RS;
+    E.p.r_st = sm_tab + 5 * RS;
+    E.p.r_plan = sm_tab + 6 * RS;
+    E.p.l_a = sm_tab + 7 * RS;
+    E.p.l_b = sm_tab + 8 * RS;
+    if (E.cfg.Rc > RS) E.cfg.Rc = RS;  // overflow -> SSB_E_CAPACITY -> host re-runs with global tables
+  }
   E.arrival = tr.arrival + I.trace_offset;
   E.prompt = tr.prompt + I.trace_offset;
   E.output = tr.output + I.trace_offset;
@@ -159,7 +177,9 @@ __global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA)
 k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, int n_order,
           int* __restrict__ queue, ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
           unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap, int64_t* ev_count) {
+  extern __shared__ int sm_engines[];
   const int lane = lane_id();
+  int* sm_tab = sm_engines + (threadIdx.x >> 5) * (SM_COLS * RS);
   while (true) {
     int q = 0;
     if (lane == 0) q = atomicAdd(queue, 1);
@@ -170,7 +190,8 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
     const Cfg cfg = make_cfg(I);
     const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers);
     Eng E;
-    bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap);
+    bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap,
+                sm_tab);
     clear_records(E, I.n_requests, lane, 32);
     fill_events(E, lane, 32);
     init_srv(E.st, cfg);
@@ -257,10 +278,11 @@ struct ClusterShared {
 };
 
 constexpr int CLUSTER_MAX_WARPS = 8;
+constexpr int CLUSTER_SMEM_SERVERS = 16;  // 16 x 9 KiB shared running tables
 
 __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr,
                           ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch,
-                          ssb_event* events, long long ev_cap, int64_t* ev_count) {
+                          ssb_event* events, long long ev_cap, int64_t* ev_count, int smem_tabs) {
   extern __shared__ long long smem_ll[];
   __shared__ ClusterShared S;
   const int idx = order[blockIdx.x];
@@ -272,6 +294,9 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   long long* v_if = smem_ll + 2 * n;   // .in_flight
   long long* rps = smem_ll + 3 * n;    // Σ prompt routed to s
   int* cnt = (int*)(smem_ll + 4 * n);  // arrivals routed to s
+  // per-server shared running tables when n servers fit (else global tables)
+  int* sm_tabs = (int*)(smem_ll + 5 * ((n + 1) & ~1));
+  const bool tabs_in_smem = smem_tabs != 0;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
   const Cfg cfg = make_cfg(I);
   const Layout L = make_layout(I.wait_cap, I.run_cap, N, n);
@@ -280,7 +305,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
   for (int s = warp; s < n; s += nwarps) {
     Eng E;
-    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap);
+    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tabs_in_smem ? sm_tabs + s * SM_COLS * RS : nullptr);
     init_srv(E.st, cfg);
     fill_events(E, lane, 32);
     if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
@@ -404,7 +429,8 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
     const double t_lim = S.t_lim;
     for (int s = warp; s < n; s += nwarps) {
       Eng E;
-      bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap);
+      bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap,
+                  tabs_in_smem ? sm_tabs + s * SM_COLS * RS : nullptr);
       Srv* sp = (Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
       E.st = *sp;
       E.advance(t_lim, cnt[s]);
@@ -545,9 +571,12 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   int* d_queue = (int*)scratch;
   if (!multis.empty()) {
     int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
-    size_t sm = sizeof(long long) * 4 * max_servers + sizeof(int) * max_servers + 16;
+    size_t sm = sizeof(long long) * 5 * ((max_servers + 1) & ~1);
+    if (max_servers <= CLUSTER_SMEM_SERVERS) sm += sizeof(int) * SM_COLS * RS * max_servers;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_cluster<<<(unsigned)multis.size(), 32 * nw, sm, stream>>>(d_inst, d_order + singles.size(), trace, records,
-                                                                d_stats, scratch, d_events, event_cap, d_event_count);
+                                                                d_stats, scratch, d_events, event_cap, d_event_count,
+                                                                max_servers <= CLUSTER_SMEM_SERVERS ? 1 : 0);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   if (!singles.empty()) {
@@ -555,10 +584,12 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engines, 32 * ENGINE_WARPS_PER_CTA, 0);
+    const size_t sm = sizeof(int) * SM_COLS * RS * ENGINE_WARPS_PER_CTA;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_engines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engines, 32 * ENGINE_WARPS_PER_CTA, sm);
     long long want = ((long long)singles.size() + ENGINE_WARPS_PER_CTA - 1) / ENGINE_WARPS_PER_CTA;
     int grid = (int)std::min<long long>(want, (long long)sms * std::max(1, occ));
-    k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, 0, stream>>>(d_inst, d_order, (int)singles.size(), d_queue, trace,
+    k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(d_inst, d_order, (int)singles.size(), d_queue, trace,
                                                               records, d_stats, scratch, d_events, event_cap,
                                                               d_event_count);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;

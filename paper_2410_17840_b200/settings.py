@@ -129,3 +129,61 @@ class ClusterSettings:
     engine: EngineSettings = field(default_factory=EngineSettings)
     balancer: BalancerSettings = field(default_factory=BalancerSettings)
     seed: int = 0
+
+
+class KvBlockPool:
+    """Host-side KV block accounting object (kvmem.py:74-154), kept for API parity
+    (Engine(pool, ...) construction, unit checks). The simulation itself keeps
+    the pool on the device as a free-block counter plus per-request
+    prompt+generated token counts (csrc/ssb_engine.cuh)."""
+
+    def __init__(self, total_blocks: int, block_size: int = DEFAULT_BLOCK_SIZE):
+        if total_blocks < 0:
+            raise ValueError(f"total_blocks must be >= 0, got {total_blocks}")
+        if block_size < 1:
+            raise ValueError(f"block_size must be >= 1, got {block_size}")
+        self.total_blocks = total_blocks
+        self.block_size = block_size
+        self.free_blocks = total_blocks
+        self._tokens: dict[int, int] = {}
+
+    def allocated_tokens(self, request_id: int) -> int:
+        return self._tokens[request_id]
+
+    def allocated_blocks(self, request_id: int) -> int:
+        return blocks_needed(self._tokens[request_id], self.block_size)
+
+    def try_allocate(self, request_id: int, tokens: int) -> bool:
+        if request_id in self._tokens:
+            raise ValueError(f"request {request_id} already holds an allocation")
+        need = blocks_needed(tokens, self.block_size)
+        if need > self.free_blocks:
+            return False
+        self._tokens[request_id] = tokens
+        self.free_blocks -= need
+        return True
+
+    def try_grow(self, request_id: int, new_total_tokens: int) -> bool:
+        if request_id not in self._tokens:
+            raise KeyError(f"request {request_id} holds no allocation")
+        current = self._tokens[request_id]
+        if new_total_tokens < current:
+            raise ValueError(f"allocation for request {request_id} cannot shrink")
+        extra = blocks_needed(new_total_tokens, self.block_size) - blocks_needed(current, self.block_size)
+        if extra > self.free_blocks:
+            return False
+        self._tokens[request_id] = new_total_tokens
+        self.free_blocks -= extra
+        return True
+
+    def free(self, request_id: int) -> int:
+        if request_id not in self._tokens:
+            raise KeyError(f"request {request_id} holds no allocation")
+        released = self.allocated_blocks(request_id)
+        del self._tokens[request_id]
+        self.free_blocks += released
+        return released
+
+    def conserved(self) -> bool:
+        held = sum(blocks_needed(t, self.block_size) for t in self._tokens.values())
+        return self.free_blocks + held == self.total_blocks and self.free_blocks >= 0

@@ -158,12 +158,45 @@ def download(db: DeviceBatch):
     return rec, stats, per
 
 
+def retry_overflows(db: DeviceBatch, stats_host: np.ndarray | None = None) -> int:
+    """Re-run, with global running tables, every instance whose shared-memory
+    running table overflowed (status SSB_E_CAPACITY). Returns the count."""
+    torch = _torch()
+    lib = _abi.load_library()
+    if stats_host is None:
+        stats_host = db.d_stats.cpu().numpy().view(_abi.STATS)
+    redo = np.flatnonzero((stats_host["status"] == _abi.SSB_E_CAPACITY)
+                          & ((db.h_inst["flags"] & _abi.SSB_FLAG_GLOBAL_TABLES) == 0))
+    if len(redo) == 0:
+        return 0
+    sub = db.h_inst[redo].copy()
+    sub["flags"] |= _abi.SSB_FLAG_GLOBAL_TABLES
+    db.h_inst["flags"][redo] |= _abi.SSB_FLAG_GLOBAL_TABLES
+    d_sub = _np_to_dev(torch, sub.view(np.uint8), db.d_inst.device)
+    d_st = torch.zeros(len(sub) * _abi.STATS.itemsize, dtype=torch.uint8, device=db.d_inst.device)
+    stream = torch.cuda.current_stream()
+    rc = lib.ssb_simulate(sub.ctypes.data, d_sub.data_ptr(), len(sub), db.trace_c(), db.records_c(),
+                          d_st.data_ptr(), db.d_scratch.data_ptr(), db.scratch_bytes, None, 0, None,
+                          ctypes.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise SimulationError(f"ssb_simulate: {lib.ssb_error_string(rc).decode()} ({rc})")
+    # scatter the re-run stats into their slots
+    rows = db.d_stats.view(len(db.h_inst), _abi.STATS.itemsize)
+    rows[torch.as_tensor(redo, device=rows.device)] = d_st.view(len(sub), _abi.STATS.itemsize)
+    db.d_inst = _np_to_dev(torch, db.h_inst.view(np.uint8), db.d_inst.device)  # later launches keep the flag
+    return len(redo)
+
+
 def run_batch(batch: Batch, *, events: bool = False, event_cap: int | None = None, check: bool = False):
     """Upload, simulate, download. Returns (records, stats[, events])."""
     torch = _torch()
     db = upload(batch, events=events, event_cap=event_cap)
     launch(db)
     torch.cuda.synchronize()
+    if retry_overflows(db):
+        if events:  # event slices are indexed by instance: re-run the whole batch
+            launch(db)
+        torch.cuda.synchronize()
     out = download(db)
     if check:
         bad = np.flatnonzero(out[1]["status"] != 0)

@@ -1,0 +1,17 @@
+"""Launch one config batch (for ncu): python tools/run_one.py c1 [reps]"""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch
+from paper_2410_17840_b200 import configs as C, instances as I, simulate
+
+which = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+jobs = {"c1": lambda: C.c1_jobs()[:1], "c1l": lambda: C.c1_jobs()[1:], "c2s": lambda: C.c2_jobs(300.0)[2:3],
+        "c3s": lambda: C.c3_jobs(20000.0)[1:], "c4": lambda: C.c4_jobs(), "c4q": lambda: C.c4_jobs(seeds=range(2)),
+        "c5s": lambda: C.c5_jobs(60.0)[:1]}[which]()
+db = simulate.upload(I.make_batch(jobs))
+for _ in range(reps):
+    simulate.launch(db)
+torch.cuda.synchronize()
+print("done", which)
