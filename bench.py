@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark: simulated request-steps/s of the BASELINE config-4 sweep.
+
+One *step* = one full policy/config sweep on each GPU: 4 policies x 4 KV
+pools x 16 arrival-rate factors x 16 seeds = 4,096 independent
+single-replica instances (~1.8k requests each, ~7.4M requests, ~1.6e9
+request-steps), simulated by the sm_100a kernels and summarised on the
+device (exact nearest-rank percentiles per instance). Weak scaling: rank r
+simulates seeds 16r..16r+15; for N>1 the per-instance summaries are
+all-gathered (NCCL) inside the step.
+
+  value : request-steps/s, inputs resident in HBM, kernels only
+  e2e   : same metric through SweepRunner.run(): pinned host -> device copy of
+          the trace + instance table, simulate, summarise, device -> host copy
+          of the per-instance stats + summaries, every step
+  --impl reference : the CPU oracle (C restatement of the reference
+          algorithm, oracle/ssb_oracle.c) on all host cores, one seed's sweep
+          (256 instances) per step.
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "simulated request-steps/sec at 1/2/4/8 B200 vs host-CPU ref; bit-exact decisions"
+UNIT = "request-steps/s"
+BYTES_PER_RSTEP = 24  # read {prompt,output,progress,kv} 16 B + write {progress,kv} 8 B
+SEEDS_PER_GPU = 16
+
+
+def config(world: int) -> dict:
+    return {
+        "workload": "C4 policy/config sweep (BASELINE.json configs[3]): {fcfs, nopreempt, trail_plus c=0.5, "
+                    "larry a=1} x KV pools {1024, 2048, 4096, 11444} x scale_qps {0.25..4.0 step 0.25} x "
+                    f"{SEEDS_PER_GPU} seeds per GPU; chat-shaped trace 3 qps, burstiness 2, 600 s per seed; "
+                    "llama3-8b/a100 cost model; 1 replica per instance",
+        "instances_per_gpu": 4 * 4 * 16 * SEEDS_PER_GPU,
+        "total_instances": 4 * 4 * 16 * SEEDS_PER_GPU * world,
+        "step": "simulate every instance + exact per-instance Summary (TTFT/nTTFT/TGT/TPOT/queue percentiles)",
+        "parallelism": f"instance-sharded x{world}" + (" + NCCL all_gather of summaries" if world > 1 else ""),
+        "l2": "working set (trace+records+scratch, ~1 GB per GPU) exceeds L2; L2 flushed (256 MB write) before "
+              "every timed step",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_hbm_peak() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+        except Exception:
+            pass
+    return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
+
+
+def ncu_traffic():
+    """dram bytes per k_engines launch from the committed ncu capture (profiles/), or None."""
+    p = ROOT / "profiles" / "r01_k_engines_traffic.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+        except Exception:
+            pass
+    return None, None
+
+
+def reference_arm(args, rank: int, world: int) -> None:
+    """--impl reference: the CPU oracle (port of the reference algorithm) on all host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200 import instances as I
+
+    O.build()
+    threads = os.cpu_count() or 1
+    batch = I.make_batch(C.c4_jobs(seeds=range(1)))
+    times, rs = [], 0
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, st = O.run_batch(batch, threads=threads)
+        dt = time.perf_counter() - t0
+        rs = int(st["request_steps"].sum())
+        if k >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = rs * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/i32", "data": "synthetic", "config": config(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "seed-0 slice of the sweep: 256 instances (4 policies x 4 pools x 16 rates), "
+                                   f"{rs:,} request-steps per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_and_parity(runner_stats) -> dict:
+    """Oracle on the host cores over the seed-0 slice (256 instances = the first 256
+    of rank 0's sweep); also checks them bit-exactly against the GPU results."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200 import instances as I
+
+    O.build()
+    threads = os.cpu_count() or 1
+    batch = I.make_batch(C.c4_jobs(seeds=range(1)))
+    t0 = time.perf_counter()
+    _, st = O.run_batch(batch, threads=threads)
+    dt = time.perf_counter() - t0
+    rs = int(st["request_steps"].sum())
+    g = runner_stats[: len(st)]
+    keys = ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "parks", "finished", "digest",
+            "status")
+    exact = all(np.array_equal(g[k], st[k]) for k in keys)
+    return {
+        "cpu_baseline": {"value": rs / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"seed-0 slice of the sweep: 256 instances, {rs:,} request-steps, {dt:.2f} s"},
+        "parity": {"instances_checked": int(len(st)), "bit_exact_vs_oracle": bool(exact),
+                   "fields": list(keys)},
+    }
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200.sweep import SweepRunner
+
+    runner = SweepRunner(C.c4_jobs(seeds=range(SEEDS_PER_GPU * rank, SEEDS_PER_GPU * (rank + 1))))
+    # first pass: correctness + overflow re-runs (deterministic: later passes identical)
+    runner.run()
+    stats, _ = runner.results()
+    overflow_reruns = runner.fix_overflows()
+    stats, summaries = runner.results()
+    if (stats["status"] != 0).any():
+        raise SystemExit(f"rank {rank}: instance status {np.unique(stats['status'])}")
+    rsteps = int(stats["request_steps"].sum())
+    gather = None
+    if world > 1:
+        gather = torch.empty(world * runner.d_summary.numel(), dtype=torch.uint8, device=runner.d_summary.device)
+
+    def step(e2e: bool):
+        runner.run(copy_inputs=e2e, read_results=False)
+        if gather is not None:
+            dist.all_gather_into_tensor(gather, runner.d_summary)
+        if e2e:
+            runner.read_results()
+
+    for _ in range(args.warmup):
+        step(False)
+        step(True)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=runner.device)
+    stream = torch.cuda.current_stream()
+
+    def timed(e2e: bool, measure_sim: bool):
+        tot = sim = 0.0
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if e2e:
+                runner.copy_inputs()
+            if measure_sim:
+                s0.record(stream)
+            runner.simulate()
+            if measure_sim:
+                s1.record(stream)
+            runner.summarize()
+            if gather is not None:
+                dist.all_gather_into_tensor(gather, runner.d_summary)
+            if e2e:
+                runner.read_results()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1) / 1e3
+            if measure_sim:
+                sim += s0.elapsed_time(s1) / 1e3
+        return tot, sim
+
+    clk = ClockSampler(local)
+    t_kernel, t_sim = timed(False, True)
+    t_e2e, _ = timed(True, False)
+    clocks = clk.stop()
+    st2, _ = runner.results()  # the e2e steps copied the results back: still the first pass's
+    assert np.array_equal(st2["digest"], stats["digest"]), "results changed between steps"
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=runner.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: int) -> int:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device=runner.device)
+        dist.all_reduce(t)
+        return int(t.item())
+
+    T_kernel, T_e2e, T_sim = max_over_ranks(t_kernel), max_over_ranks(t_e2e), max_over_ranks(t_sim)
+    total_rsteps = sum_over_ranks(rsteps)
+    if rank == 0:
+        K = args.steps
+        value = total_rsteps * K / T_kernel
+        e2e_value = total_rsteps * K / T_e2e
+        sim_s = T_sim / K
+        achieved = BYTES_PER_RSTEP * rsteps / sim_s / 1e9  # per launch on this rank
+        peak, peak_src = measured_hbm_peak()
+        traffic, _alg = ncu_traffic()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": 1e3 * T_kernel / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/i32", "data": "synthetic", "config": config(world),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(runner.h2d_bytes),
+                    "d2h_bytes_per_step": int(runner.d2h_bytes), "ms_per_step": 1e3 * T_e2e / K,
+                    "api": "paper_2410_17840_b200.sweep.SweepRunner.run"},
+            "roofline": {"bound": "hbm", "kernel": "k_engines (ssb_simulate)", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": f"{BYTES_PER_RSTEP} B/request-step x {rsteps:,} request-steps",
+                         "kernel_ms": 1e3 * sim_s, "kernel_share_of_step": sim_s / (T_kernel / K),
+                         "peak_source": peak_src},
+            "gpu_launches": runner.launches_per_run * K * 2,
+            "clocks": clocks,
+            "request_steps_per_gpu_step": rsteps,
+            "requests_per_gpu_step": int(runner.batch.n_records),
+            "overflow_reruns": overflow_reruns,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line.update(cpu_baseline_and_parity(stats))
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
