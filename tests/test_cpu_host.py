@@ -1,0 +1,174 @@
+"""CPU-only checks: the C ABI library's symbols/layouts, the host-side mirror of
+the reference interface (settings, registries, feasibility, synthesis, RNG
+model) and the reference's own known-answer tests for the pure functions."""
+
+import ctypes
+import json
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2410_17840_b200 as P
+from golden_util import trace_sha
+from helpers import load_golden, scenario_trace
+from oracle import oracle as O
+import scenarios as S
+from paper_2410_17840_b200 import _abi
+from paper_2410_17840_b200 import instances as I
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _header_functions():
+    text = (ROOT / "include" / "ssb.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int32_t|size_t|const char\*)\s+(ssb_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2410_17840_b200 import build as B
+
+    B.build()
+    lib = ctypes.CDLL(str(_abi.LIB_PATH))
+    names = _header_functions()
+    assert len(names) >= 7, names
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_abi.EXPORTS), (set(names) ^ set(_abi.EXPORTS))
+
+
+def test_struct_layouts_match_numpy_mirror():
+    lib = _abi.load_library()
+    assert lib.ssb_abi_version() == 1
+    assert lib.ssb_error_string(3) == b"device table capacity exceeded"
+
+
+def test_prepare_plans_capacities():
+    lib = _abi.load_library()
+    tr = P.synthesize(P.SynthSpec(duration_s=50, mean_qps=3, seed=1))
+    b = I.make_batch([(P.ClusterSettings(1, P.EngineSettings(pool_blocks=700, max_running=9)), tr, 1.0),
+                      (P.ClusterSettings(3, P.EngineSettings(pool_blocks=50000)), tr, 2.0)])
+    inst = b.instances.copy()
+    total = lib.ssb_prepare(inst.ctypes.data, len(inst))
+    assert inst[0]["run_cap"] == 9 and inst[0]["wait_cap"] == len(tr)
+    assert inst[1]["run_cap"] == len(tr)
+    assert inst[1]["scratch_offset"] > inst[0]["scratch_offset"] and total > inst[1]["scratch_offset"]
+
+
+def test_synthesize_is_bit_identical_to_reference():
+    golden = load_golden("configs")
+    for sc in S.config_scenarios():
+        t = scenario_trace(sc)
+        arr = t.arrival / sc["qps_factor"]
+        assert trace_sha(arr, t.prompt, t.output) == golden[sc["name"]]["trace_sha"], sc["name"]
+
+
+def test_pcg64_model_matches_numpy():
+    for seed in (0, 3, 9, 123456789):
+        words = P.balancers.pcg64_words(seed)
+        highs = np.array([2, 3, 8, 64, 1, 7, 2, 1, 5] * 50, dtype=np.int64)
+        got = O.rng_integers(words, highs)
+        rng = np.random.default_rng(seed)
+        want = np.array([int(rng.integers(int(h))) for h in highs])
+        assert np.array_equal(got, want), seed
+
+
+def test_settings_resolution():
+    re_ = I.resolve_engine(P.EngineSettings(profile="llama3-70b", hardware="h100x2", gpu_mem_bytes=160e9))
+    assert re_.pool_blocks == 17166
+    assert I.resolve_engine(P.EngineSettings()).pool_blocks == 11444  # test_kvmem.py:45
+    assert P.pool_blocks_for(40e9, P.PROFILES["llama3-8b"]) == 11444
+    assert P.blocks_needed(2000, 16) == 125
+    with pytest.raises(ValueError):
+        P.make_policy("sjf")
+    with pytest.raises(ValueError):
+        P.make_policy("trail_plus", c=1.5)
+    with pytest.raises(ValueError):
+        I.instance_record(P.ClusterSettings(balancer=P.BalancerSettings(poll_interval_s=0.0)), 1)
+
+
+def test_feasibility_errors_match_reference_messages():
+    golden_msgs = {
+        (2000, 7000): "request 0: prompt 2000 + output 7000 exceeds the 8192-token context window",
+    }
+    for (p, o), msg in golden_msgs.items():
+        with pytest.raises(P.InfeasibleRequestError, match=re.escape(msg)):
+            I.check_trace(P.Trace([0.0], [p], [o]), I.resolve_engine(P.EngineSettings()))
+    with pytest.raises(P.InfeasibleRequestError, match="needs 7 blocks at peak, pool holds 4"):
+        I.check_trace(P.Trace([0.0], [100], [10]), I.resolve_engine(P.EngineSettings(pool_blocks=4)))
+    np_ = I.resolve_engine(P.EngineSettings(policy="nopreempt", max_output=20))
+    with pytest.raises(P.InfeasibleRequestError, match="exceeds the promised max_output 20"):
+        I.check_trace(P.Trace([0.0, 1.0], [10, 10], [5, 30]), np_)
+    with pytest.raises(ValueError, match="sorted"):
+        I.check_trace(P.Trace([1.0, 0.5], [10, 10], [1, 1]), I.resolve_engine(P.EngineSettings()))
+
+
+def test_custom_python_policies_are_rejected():
+    class MyPolicy(P.FcfsPolicy):
+        pass
+
+    with pytest.raises(NotImplementedError):
+        P.policies.policy_descriptor(MyPolicy())
+    with pytest.raises(NotImplementedError):
+        P.FcfsPolicy().select([], [], None, 0.0, None)
+
+
+def test_reference_pure_function_kats():
+    # larry_score (test_policies.py:51-55)
+    class R:
+        enqueue_time = 0.0
+        pending_prefill = 512
+
+    assert P.larry_score(R, 10.0, 4, 1.0) == -2038.0
+    assert P.larry_score(R, 10.0, 4, 1000.0) == 7952.0
+    # sal_load / beta (test_balancers.py:85-96, 157-165)
+    beta = 1365 / 211
+    assert P.sal_load(P.ServerStats(1536, 0, 3), 1024, beta, 1024) == beta * 1024
+    assert P.sal_load(P.ServerStats(128, 10**6, 1), 128, 2.0, 1024) == 256 / 1024
+    est = P.BetaEstimator()
+    for _ in range(40):
+        est.update(1154, 211)
+    assert est.beta == 1365 / 211
+    # nearest-rank percentile (test_metrics.py:17-31)
+    v = list(range(1, 101))
+    assert [P.percentile(v, p) for p in (50, 95, 99, 100, 1, 0.5)] == [50, 95, 99, 100, 1, 1]
+    assert P.percentile([3, 1, 2], 67) == 3
+    assert P.metrics.nearest_ranks(10_000_000) == (5_000_000, 9_500_000, 9_900_000)
+
+
+def test_kv_block_pool_conserves_memory():
+    """criterion 7 (test_acceptance.py:344-368) on the host mirror."""
+    rng = np.random.default_rng(4107)
+    pool = P.KvBlockPool(64, 8)
+    live, next_id = [], 0
+    for _ in range(20_000):
+        roll = rng.random()
+        if live and (roll < 0.2 or len(live) >= 50):
+            pool.free(live.pop(int(rng.integers(len(live)))))
+        elif live and roll < 0.5:
+            rid = live[int(rng.integers(len(live)))]
+            pool.try_grow(rid, pool.allocated_tokens(rid) + int(rng.integers(1, 65)))
+        else:
+            if pool.try_allocate(next_id, int(rng.integers(1, 301))):
+                live.append(next_id)
+            next_id += 1
+        assert pool.free_blocks >= 0 and pool.conserved()
+
+
+def test_writers_are_byte_stable(tmp_path):
+    recs = [P.MetricsRecord(i, 0, i * 0.1, i * 0.1 + 0.37, i * 0.1 + 1.0, 100, 10, 0) for i in range(5)]
+    P.write_records_csv(tmp_path / "a.csv", recs)
+    P.write_records_csv(tmp_path / "b.csv", recs)
+    assert (tmp_path / "a.csv").read_bytes() == (tmp_path / "b.csv").read_bytes()
+    assert (tmp_path / "a.csv").read_text().splitlines()[2] == "1,0,0.1,0.47,1.1,100,10,0"
+
+
+def test_simulation_path_fails_loudly_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    with pytest.raises(Exception, match="CUDA"):
+        P.run_cluster(P.ClusterSettings(), [P.TraceEntry(0.0, 10, 1)])
