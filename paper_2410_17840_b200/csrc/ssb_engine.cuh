@@ -131,6 +131,37 @@ __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool
   return warp_argmax_u64(~key, has);
 }
 
+// ceil(t / bs) for block sizes that are not a power of two (kept out of line:
+// the integer division would otherwise be inlined at every call site)
+__device__ __noinline__ int div_up_slow(int t, int bs) { return (t + bs - 1) / bs; }
+
+// stable compaction of a running table (drops ST_GONE entries); returns the new size.
+// Out of line with pointer/int arguments only, so callers keep their state in registers.
+__device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restrict__ r_prompt, int* __restrict__ r_out,
+                                          int* __restrict__ r_gen, int* __restrict__ r_pfd, int* __restrict__ r_st, int R) {
+  const int lane = threadIdx.x & 31;
+  int out = 0;
+  for (int base = 0; base < R; base += 32) {
+    const int j = base + lane;
+    const bool valid = j < R;
+    int rid = 0, pr = 0, o = 0, g = 0, f = 0, s = ST_GONE;
+    if (valid) {
+      s = r_st[j];
+      rid = r_rid[j]; pr = r_prompt[j]; o = r_out[j]; g = r_gen[j]; f = r_pfd[j];
+    }
+    const bool keep = valid && s != ST_GONE;
+    const unsigned m = __ballot_sync(FULL, keep);
+    __syncwarp();
+    if (keep) {
+      const int d = out + __popc(m & lanemask_lt());
+      r_rid[d] = rid; r_prompt[d] = pr; r_out[d] = o; r_gen[d] = g; r_pfd[d] = f; r_st[d] = s;
+    }
+    out += __popc(m);
+    __syncwarp();
+  }
+  return out;
+}
+
 struct Eng {
   Cfg cfg;
   Srv st;
@@ -147,9 +178,44 @@ struct Eng {
   long long ev_cap;
   int server;
   int lane;
+  // steady-state decode mode: running entries j = lane and j = lane + 32 cached in
+  // registers across iterations (valid when regs_ok), rsum = Σ (prompt+generated)
+  int c_rid0, c_pr0, c_out0, c_g0, c_rid1, c_pr1, c_out1, c_g1;
+  bool regs_ok, regs_dirty;
+  long long rsum;
+  // nodisp: the last select dispatched nothing and nothing it depends on has
+  // changed since (no enqueue / dispatch / finish / preempt) -> it would again
+  // dispatch nothing: FCFS & NoPreempt (free only shrinks, committed fixed),
+  // trail_plus (free + coverable victim blocks never grows), any policy with W == 0.
+  bool nodisp;
+
+  __device__ __forceinline__ void init_modes() { regs_ok = regs_dirty = false; rsum = 0; nodisp = false; }
+  __device__ __forceinline__ void flush_regs() {
+    if (regs_dirty) {
+      if (lane < st.R) p.r_gen[lane] = c_g0;
+      if (lane + 32 < st.R) p.r_gen[lane + 32] = c_g1;
+      regs_dirty = false;
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ void drop_regs() {
+    flush_regs();
+    regs_ok = false;
+  }
+  __device__ __forceinline__ void load_regs() {
+    const bool v0 = lane < st.R, v1 = lane + 32 < st.R;
+    c_rid0 = c_pr0 = c_out0 = c_g0 = c_rid1 = c_pr1 = c_out1 = c_g1 = 0;
+    if (v0) { c_rid0 = p.r_rid[lane]; c_pr0 = p.r_prompt[lane]; c_out0 = p.r_out[lane]; c_g0 = p.r_gen[lane]; }
+    if (v1) {
+      c_rid1 = p.r_rid[lane + 32]; c_pr1 = p.r_prompt[lane + 32]; c_out1 = p.r_out[lane + 32]; c_g1 = p.r_gen[lane + 32];
+    }
+    rsum = (long long)redux_add(v0 ? c_pr0 + c_g0 : 0) + redux_add(v1 ? c_pr1 + c_g1 : 0);
+    regs_ok = true;
+    regs_dirty = false;
+  }
 
   __device__ __forceinline__ int blocks(int tokens) const {  // kvmem.py:15-21
-    return cfg.bs_shift >= 0 ? (tokens + cfg.bs - 1) >> cfg.bs_shift : (tokens + cfg.bs - 1) / cfg.bs;
+    return cfg.bs_shift >= 0 ? (tokens + cfg.bs - 1) >> cfg.bs_shift : div_up_slow(tokens, cfg.bs);
   }
   __device__ __forceinline__ int phys(int k) const {  // ring slot of logical position k
     int x = st.whead + k;
@@ -248,6 +314,7 @@ struct Eng {
         rec_srv[rid] = server;
       }
       emit(m, SSB_EV_ENQUEUE, rid);
+      nodisp = false;
       long long s = warp_sum_ll(pr);
       st.W += cnt;
       st.wpend_sum += s;
@@ -261,6 +328,7 @@ struct Eng {
   // ---- push a running entry back to the waiting head (_preempt, engine.py:368-379) ----
   // uniform call; the entry is table index j with loaded fields
   __device__ void preempt_entry(int j, int rid, int pr, int out, int gen, int pfd, int state, int code) {
+    nodisp = false;
     int alloc = pr + gen;  // KV tokens held
     st.free_blocks += blocks(alloc);
     if (state == ST_DECODE) st.ndec -= 1;
@@ -285,27 +353,8 @@ struct Eng {
   }
 
   // ---- stable compaction of the running table (drops ST_GONE) ----
-  __device__ void compact_running() {
-    int out = 0;
-    for (int base = 0; base < st.R; base += 32) {
-      int j = base + lane;
-      bool valid = j < st.R;
-      int rid = 0, pr = 0, o = 0, g = 0, f = 0, s = ST_GONE;
-      if (valid) {
-        s = p.r_st[j];
-        rid = p.r_rid[j]; pr = p.r_prompt[j]; o = p.r_out[j]; g = p.r_gen[j]; f = p.r_pfd[j];
-      }
-      bool keep = valid && s != ST_GONE;
-      unsigned m = __ballot_sync(FULL, keep);
-      __syncwarp();
-      if (keep) {
-        int d = out + __popc(m & lanemask_lt());
-        p.r_rid[d] = rid; p.r_prompt[d] = pr; p.r_out[d] = o; p.r_gen[d] = g; p.r_pfd[d] = f; p.r_st[d] = s;
-      }
-      out += __popc(m);
-      __syncwarp();
-    }
-    st.R = out;
+  __device__ __forceinline__ void compact_running() {
+    st.R = compact_table(p.r_rid, p.r_prompt, p.r_out, p.r_gen, p.r_pfd, p.r_st, st.R);
   }
 
   // ---- FCFS / NoPreempt: dispatch the longest fitting queue prefix ----
@@ -572,6 +621,7 @@ struct Eng {
   // ---- apply dispatches (engine.py:287-298) in decision order ----
   __device__ void apply_dispatches(int nd, bool prefix_mode) {
     if (nd == 0) return;
+    nodisp = false;
     if (st.R + nd > cfg.Rc) { st.status = SSB_E_CAPACITY; return; }
     int need_sum = 0;
     long long pend_sum = 0;
@@ -745,6 +795,7 @@ struct Eng {
       int n_fin = __popc(m_fin);
       st.ndec += __popc(m_dec_in) - n_fin;
       if (n_fin) {
+        nodisp = false;
         removed_any = true;
         st.finished += n_fin;
         st.fin_cnt += n_fin;
@@ -789,6 +840,7 @@ struct Eng {
           if (lane == 0) { p.r_gen[j] = fg + 1; if (ffin) p.r_st[j] = ST_GONE; }
         }
         if (ffin) {
+          nodisp = false;
           if (lane == 0) rec_fin[frid] = st.clock;
           st.free_blocks += PREFILL ? blocks(fpr + 1) : blocks(fpr + fg + 1);
           emit1(SSB_EV_FINISH, frid);
@@ -895,6 +947,7 @@ struct Eng {
     st.pf_pend -= pf_tokens;
     st.ndec += __popc(m_first | m_rec) - __popc(m_fin);
     if (m_fin) {
+      nodisp = false;
       const int nf = __popc(m_fin);
       st.finished += nf;
       st.fin_cnt += nf;
@@ -919,19 +972,85 @@ struct Eng {
     st.iterations += 1;
   }
 
+  // ---- steady-state decode iteration (engine.py:300-357 specialised) ----
+  // Preconditions (checked by step): every running request is DECODING,
+  // R <= min(64, cap) so the plan is "one token each, table order", block size a
+  // power of two. The KV resident sum is maintained incrementally; grows cross a
+  // block boundary iff (prompt+generated) % bs == 0. If the plan's grow demand does
+  // not fit the free pool, returns false with nothing modified (ordered path).
+  __device__ bool fast_decode() {
+    const int R = st.R;
+    const int bsm = cfg.bs - 1;
+    const bool v0 = lane < R, v1 = lane + 32 < R;
+    const bool x0 = v0 && ((c_pr0 + c_g0) & bsm) == 0;
+    const bool x1 = v1 && ((c_pr1 + c_g1) & bsm) == 0;
+    const int need = __popc(__ballot_sync(FULL, x0)) + __popc(__ballot_sync(FULL, x1));
+    if (need > st.free_blocks) return false;
+    {  // iteration_latency (costmodel.py:45-47); clock += latency (engine.py:219-220)
+      const double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, (double)rsum));
+      const double comp = __dmul_rn(cfg.compute, (double)R);
+      st.clock = __dadd_rn(st.clock, __dadd_rn(cfg.overhead, comp > mem ? comp : mem));
+    }
+    c_g0 += v0;
+    c_g1 += v1;
+    regs_dirty = true;
+    rsum += R;
+    st.free_blocks -= need;
+    st.rsteps += R;
+    st.btokens += R;
+    if (R > st.peak) st.peak = R;
+    st.iterations += 1;
+    const bool f0 = v0 && c_g0 == c_out0, f1 = v1 && c_g1 == c_out1;
+    const unsigned m0 = __ballot_sync(FULL, f0), m1 = __ballot_sync(FULL, f1);
+    if (m0 | m1) finish_fast(f0, f1, m0, m1);
+    return true;
+  }
+
+  // finishes inside a steady-state iteration (_finish, engine.py:360-366)
+  __device__ void finish_fast(bool f0, bool f1, unsigned m0, unsigned m1) {
+    nodisp = false;
+    if (f0) rec_fin[c_rid0] = st.clock;
+    if (f1) rec_fin[c_rid1] = st.clock;
+    emit(m0, SSB_EV_FINISH, c_rid0);  // decode plan order == table order
+    emit(m1, SSB_EV_FINISH, c_rid1);
+    const int n = __popc(m0) + __popc(m1);
+    st.free_blocks += redux_add(f0 ? blocks(c_pr0 + c_g0) : 0) + redux_add(f1 ? blocks(c_pr1 + c_g1) : 0);
+    st.finished += n;
+    st.fin_cnt += n;
+    st.fin_in += redux_add(f0 ? c_pr0 : 0) + redux_add(f1 ? c_pr1 : 0);
+    st.fin_out += redux_add(f0 ? c_out0 : 0) + redux_add(f1 ? c_out1 : 0);
+    if (cfg.policy == SSB_POLICY_NOPREEMPT)
+      st.committed -= redux_add(f0 ? wkey_for(c_pr0, c_out0, 0) : 0) + redux_add(f1 ? wkey_for(c_pr1, c_out1, 0) : 0);
+    st.ndec -= n;
+    if (lane < st.R) { p.r_gen[lane] = c_g0; if (f0) p.r_st[lane] = ST_GONE; }
+    if (lane + 32 < st.R) { p.r_gen[lane + 32] = c_g1; if (f1) p.r_st[lane + 32] = ST_GONE; }
+    regs_ok = regs_dirty = false;
+    __syncwarp();
+    compact_running();
+  }
+
   // ---- Engine.step (engine.py:193-234) ----
   __device__ void step() {
     if (!has_work()) { st.status = SSB_E_STALL; return; }
     int nd = 0, np = 0;
     bool prefix = false;
-    switch (cfg.policy) {
-      case SSB_POLICY_FCFS:
-      case SSB_POLICY_NOPREEMPT: nd = select_prefix(); prefix = true; break;
-      case SSB_POLICY_TRAIL_PLUS: select_trail(nd, np); break;
-      case SSB_POLICY_LARRY: nd = select_larry(); break;
-      default: st.status = SSB_E_ARG; return;
+    if (!nodisp) {
+      switch (cfg.policy) {
+        case SSB_POLICY_FCFS:
+        case SSB_POLICY_NOPREEMPT: nd = select_prefix(); prefix = true; break;
+        case SSB_POLICY_TRAIL_PLUS:
+          if (cfg.c != 0.0) flush_regs();  // victims read the table
+          select_trail(nd, np);
+          break;
+        case SSB_POLICY_LARRY: nd = select_larry(); break;
+        default: st.status = SSB_E_ARG; return;
+      }
+      // nothing dispatched: stays so until an enqueue / dispatch / finish / preempt
+      // (larry's order moves with the clock, so only an empty queue is stable)
+      if (nd == 0 && np == 0) nodisp = cfg.policy != SSB_POLICY_LARRY || st.W == 0;
     }
     if (np > 0) {  // policy preempts first (engine.py:203-204), in decision order
+      drop_regs();
       for (int t = 0; t < np; ++t) {
         int j = p.l_b[t];
         int vs = p.r_st[j], vrid = p.r_rid[j], vpr = p.r_prompt[j], vout = p.r_out[j], vg = p.r_gen[j],
@@ -940,8 +1059,16 @@ struct Eng {
       }
       compact_running();
     }
-    apply_dispatches(nd, prefix);  // then dispatches (engine.py:205-206)
-    if (st.status) return;
+    if (nd > 0) {
+      drop_regs();
+      apply_dispatches(nd, prefix);  // then dispatches (engine.py:205-206)
+      if (st.status) return;
+    }
+    if (st.R > 0 && st.R <= 64 && st.ndec == st.R && st.R <= cfg.cap && cfg.bs_shift >= 0) {
+      if (!regs_ok) load_regs();
+      if (fast_decode()) return;
+    }
+    drop_regs();
     if (st.R <= 32) { batch_progress_small(); return; }
     int total, nent, npf;
     long long resident;
@@ -967,6 +1094,7 @@ struct Eng {
     return arrival_of(rid);
   }
   __device__ void advance(double t_lim, int n_avail) {
+    init_modes();
     double next_t = next_arrival(n_avail);
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
     while (st.status == SSB_OK) {
@@ -986,6 +1114,7 @@ struct Eng {
       }
       step();
     }
+    drop_regs();  // the table in memory is authoritative between calls
   }
 };
 
