@@ -71,9 +71,11 @@ struct SrvPtr {
   int* r_plan;
   int* l_a;   // dispatch list (physical ring slots) / scratch list
   int* l_b;   // preempt list (table indices) / scratch list
+  int* l_c;   // trail_plus dispatch list: pending prefill
   int* v_idx; // trail_plus victims sorted by (-remaining, -dispatch_seq)
   int* v_rem;
   long long* v_cum;
+  unsigned long long* v_key;  // unsorted compact victim keys (scratch)
   int* rl;    // route list (arrival ids routed to this engine), n_servers > 1
 };
 
@@ -288,6 +290,58 @@ struct Eng {
     st.ev_n += 1;
   }
 
+  // ---- trail_plus waiting set: slots [0, W) sorted by key = (remaining << 32 | id) ----
+  // (whead stays 0; the 64-bit key lives in the w_enq column, rid|flag in w_rid, pending in w_pend)
+  __device__ __forceinline__ unsigned long long* wkey64() const { return reinterpret_cast<unsigned long long*>(p.w_enq); }
+  __device__ int trail_lower_bound(unsigned long long k, int n) const {  // first slot with key >= k
+    int lo = 0, hi = n;
+    while (hi - lo > 32) {  // 32-ary search: one ballot per level
+      const int step = (hi - lo + 31) >> 5;
+      const int pos = lo + lane * step;
+      const unsigned m = __ballot_sync(FULL, pos < hi && wkey64()[pos] < k);
+      const int c = __popc(m);
+      const int nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
+      const int nhi = min(hi, lo + c * step);
+      lo = nlo;
+      hi = nhi;
+    }
+    const int pos = lo + lane;
+    return lo + __popc(__ballot_sync(FULL, pos < hi && wkey64()[pos] < k));
+  }
+  __device__ void trail_insert(int rid_flag, int pend, int rem) {
+    const unsigned long long k = ((unsigned long long)(unsigned)rem << 32) | (unsigned)(rid_flag & 0x7fffffff);
+    const int n = st.W;
+    if (n + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
+    const int pos = trail_lower_bound(k, n);
+    for (int hi = n; hi > pos; hi -= 32) {  // shift [pos, n) up one slot, top chunk first
+      const int lo = max(pos, hi - 32);
+      const int i = lo + lane;
+      const bool v = i < hi;
+      unsigned long long kk = 0;
+      int r = 0, pd = 0;
+      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
+      __syncwarp();
+      if (v) { wkey64()[i + 1] = kk; p.w_rid[i + 1] = r; p.w_pend[i + 1] = pd; }
+      __syncwarp();
+    }
+    if (lane == 0) { wkey64()[pos] = k; p.w_rid[pos] = rid_flag; p.w_pend[pos] = pend; }
+    __syncwarp();
+    st.W = n + 1;
+  }
+  __device__ void trail_remove(int pos) {  // shift (pos, W) down one slot
+    for (int lo = pos + 1; lo < st.W; lo += 32) {
+      const int i = lo + lane;
+      const bool v = i < st.W;
+      unsigned long long kk = 0;
+      int r = 0, pd = 0;
+      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
+      __syncwarp();
+      if (v) { wkey64()[i - 1] = kk; p.w_rid[i - 1] = r; p.w_pend[i - 1] = pd; }
+      __syncwarp();
+    }
+    st.W -= 1;
+  }
+
   // ---- Engine.enqueue for every routed arrival with arrival <= clock (engine.py:175-184, 261-262) ----
   __device__ void enqueue_ready(int n_avail) {
     while (st.next_arr < n_avail) {
@@ -304,19 +358,29 @@ struct Eng {
       if (cnt == 0) break;
       if (st.W + cnt > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
       int pr = 0;
+      const bool trail = cfg.policy == SSB_POLICY_TRAIL_PLUS;
       if (ok) {
         pr = prompt[rid];
-        int pos = phys(st.W + lane);
-        p.w_rid[pos] = rid;
-        p.w_pend[pos] = pr;
-        p.w_key[pos] = wkey_for(pr, output[rid], 0);
-        p.w_enq[pos] = st.clock;
         rec_srv[rid] = server;
+        if (!trail) {
+          int pos = phys(st.W + lane);
+          p.w_rid[pos] = rid;
+          p.w_pend[pos] = pr;
+          p.w_key[pos] = wkey_for(pr, output[rid], 0);
+          p.w_enq[pos] = st.clock;
+        }
+      }
+      if (trail) {  // sorted by (remaining, id): insert in arrival order
+        const int out = ok ? output[rid] : 0;
+        for (unsigned mm = m; mm; mm &= mm - 1) {
+          const int b = __ffs(mm) - 1;
+          trail_insert(__shfl_sync(FULL, rid, b), __shfl_sync(FULL, pr, b), __shfl_sync(FULL, out, b));
+        }
       }
       emit(m, SSB_EV_ENQUEUE, rid);
       nodisp = false;
       long long s = warp_sum_ll(pr);
-      st.W += cnt;
+      if (!trail) st.W += cnt;
       st.wpend_sum += s;
       st.enq_prompt_sum += s;
       st.next_arr += cnt;
@@ -335,17 +399,23 @@ struct Eng {
     else st.pf_pend -= (long long)(alloc - pfd);
     if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= wkey_for(pr, out, gen);
     if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
-    st.whead = (st.whead == 0) ? cfg.Wc - 1 : st.whead - 1;
-    if (lane == 0) {
-      int pos = st.whead;
-      p.w_rid[pos] = rid | FLAG_SEEN;
-      p.w_pend[pos] = alloc;  // pending_prefill = prompt + generated (prefill_done reset)
-      p.w_key[pos] = wkey_for(pr, out, gen);
-      p.w_enq[pos] = st.clock;
-      p.r_st[j] = ST_GONE;
-      rec_pc[rid] += 1;
+    if (cfg.policy == SSB_POLICY_TRAIL_PLUS) {  // sorted waiting set: order is by key, not by deque position
+      if (lane == 0) { p.r_st[j] = ST_GONE; rec_pc[rid] += 1; }
+      __syncwarp();
+      trail_insert(rid | FLAG_SEEN, alloc, out - gen);
+    } else {
+      st.whead = (st.whead == 0) ? cfg.Wc - 1 : st.whead - 1;
+      if (lane == 0) {
+        int pos = st.whead;
+        p.w_rid[pos] = rid | FLAG_SEEN;
+        p.w_pend[pos] = alloc;  // pending_prefill = prompt + generated (prefill_done reset)
+        p.w_key[pos] = wkey_for(pr, out, gen);
+        p.w_enq[pos] = st.clock;
+        p.r_st[j] = ST_GONE;
+        rec_pc[rid] += 1;
+      }
+      st.W += 1;
     }
-    st.W += 1;
     st.wpend_sum += alloc;
     if (code == SSB_EV_PARK) st.parks += 1; else st.preempts += 1;
     emit1(code, rid);
@@ -448,40 +518,33 @@ struct Eng {
   }
 
   // ---- trail_plus victims: eligible running entries sorted by (-remaining, -dispatch_seq) ----
+  // eligible = unmarked (r_plan == 0) and generated < c * output_len (policies.py:190-196).
+  // Compact 64-bit keys (remaining << 32 | table index) -> rank sort -> prefix block sums.
+  __device__ __forceinline__ bool victim_eligible(int j, int& g, int& o) const {
+    if (p.r_plan[j] != 0) return false;
+    g = p.r_gen[j];
+    o = p.r_out[j];
+    return (double)g < __dmul_rn(cfg.c, (double)o);
+  }
   __device__ int build_victims() {
-    // eligible: unmarked (r_plan == 0) and generated < c * output_len (policies.py:190-196)
     int V = 0;
     for (int base = 0; base < st.R; base += 32) {
-      int j = base + lane;
-      bool e = false;
-      if (j < st.R) e = p.r_plan[j] == 0 && (double)p.r_gen[j] < __dmul_rn(cfg.c, (double)p.r_out[j]);
-      V += __popc(__ballot_sync(FULL, e));
+      const int j = base + lane;
+      int g = 0, o = 0;
+      const bool e = j < st.R && victim_eligible(j, g, o);
+      const unsigned m = __ballot_sync(FULL, e);
+      if (e) p.v_key[V + __popc(m & lanemask_lt())] = ((unsigned long long)(unsigned)(o - g) << 32) | (unsigned)j;
+      V += __popc(m);
     }
-    // rank sort: rank(v) = #{u eligible : key_u > key_v}, key = (remaining << 32) | idx
-    for (int base = 0; base < st.R; base += 32) {
-      int j = base + lane;
-      bool e = false;
-      unsigned long long kv = 0;
-      int rem = 0, blk = 0;
-      if (j < st.R) {
-        e = p.r_plan[j] == 0 && (double)p.r_gen[j] < __dmul_rn(cfg.c, (double)p.r_out[j]);
-        rem = p.r_out[j] - p.r_gen[j];
-        blk = blocks(p.r_prompt[j] + p.r_gen[j]);
-        kv = ((unsigned long long)(unsigned)rem << 32) | (unsigned)j;
-      }
-      if (e) {
-        int rank = 0;
-        for (int u = 0; u < st.R; ++u) {
-          if (p.r_plan[u] != 0) continue;
-          int gu = p.r_gen[u], ou = p.r_out[u];
-          if (!((double)gu < __dmul_rn(cfg.c, (double)ou))) continue;
-          unsigned long long ku = ((unsigned long long)(unsigned)(ou - gu) << 32) | (unsigned)u;
-          rank += ku > kv;
-        }
-        p.v_idx[rank] = j;
-        p.v_rem[rank] = rem;
-        p.v_cum[rank] = blk;  // prefix-summed below
-      }
+    __syncwarp();
+    for (int i = lane; i < V; i += 32) {  // descending key == (-remaining, -dispatch_seq)
+      const unsigned long long k = p.v_key[i];
+      int rank = 0;
+      for (int u = 0; u < V; ++u) rank += p.v_key[u] > k;
+      const int j = (int)(unsigned)k;
+      p.v_idx[rank] = j;
+      p.v_rem[rank] = (int)(k >> 32);
+      p.v_cum[rank] = blocks(p.r_prompt[j] + p.r_gen[j]);
     }
     __syncwarp();
     long long carry = 0;
@@ -495,6 +558,17 @@ struct Eng {
     __syncwarp();
     return V;
   }
+  // Σ allocated blocks over eligible victims: an upper bound of any candidate's gain
+  __device__ long long victims_total() const {
+    long long t = 0;
+    for (int base = 0; base < st.R; base += 32) {
+      const int j = base + lane;
+      int g = 0, o = 0;
+      const bool e = j < st.R && victim_eligible(j, g, o);
+      t += redux_add(e ? blocks(p.r_prompt[j] + g) : 0);
+    }
+    return t;
+  }
   // number of victims with remaining > r (a prefix of the sorted list)
   __device__ __forceinline__ int victims_above(int V, int r) const {
     int lo = 0, hi = V;
@@ -506,7 +580,13 @@ struct Eng {
   }
 
   // ---- trail_plus (policies.py:168-212): greedy skip in (remaining, arrival, id) order ----
-  // arrival order == id order (trace sorted, ids in trace order), so the key is (remaining, id).
+  // arrival order == id order (trace sorted, ids in trace order), so the key is (remaining, id)
+  // and the waiting set is kept sorted by it. The walk visits 32 candidates per step: a
+  // candidate is actionable if it fits the free pool or (c > 0) the victims can cover it;
+  // the first actionable one is taken (dispatch, possibly after choosing victims), removed
+  // from the set, and the walk resumes at the same slot with the updated free pool/marks.
+  // Victims are only sorted when a blocked candidate passes the cheap upper bound
+  // need <= free + Σ(eligible blocks). Dispatches go to l_a (rid|flag) / l_c (pending).
   __device__ void select_trail(int& nd_out, int& np_out) {
     int nd = 0, np = 0;
     if (st.W == 0) { nd_out = np_out = 0; return; }
@@ -515,58 +595,86 @@ struct Eng {
       for (int j = lane; j < st.R; j += 32) p.r_plan[j] = 0;  // marks
     __syncwarp();
     int free = st.free_blocks;
-    unsigned long long last = 0;  // keys are >= 1<<32 (remaining >= 1)
     int V = -1;
-    while (true) {
+    int vr = 0x7fffffff;  // victims held in registers when V <= 32: lane v has (remaining, cumulative blocks)
+    long long vc = 0;
+    int k0 = 0;
+    while (k0 < st.W) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;
-      if (can_preempt && V < 0) V = build_victims();
-      unsigned long long best = ~0ULL;
-      int best_k = -1;
-      for (int k = lane; k < st.W; k += 32) {
-        int pos = phys(k);
-        int rid = p.w_rid[pos] & 0x7fffffff;
-        int rem = p.w_key[pos];
-        unsigned long long key = ((unsigned long long)(unsigned)rem << 32) | (unsigned)rid;
-        if (key <= last || key >= best) continue;
-        int need = blocks(p.w_pend[pos]);
-        bool ok = need <= free;
-        if (!ok && can_preempt) {
-          int m = victims_above(V, rem);
-          long long gain = m > 0 ? p.v_cum[m - 1] : 0;
-          ok = (long long)free + gain >= need;
+      const int k = k0 + lane;
+      const bool v = k < st.W;
+      unsigned long long key = 0;
+      int pend = 0, need = 0;
+      if (v) { key = wkey64()[k]; pend = p.w_pend[k]; need = blocks(pend); }
+      const int rem = (int)(key >> 32);
+      const bool fit = v && need <= free;
+      const unsigned mfit = __ballot_sync(FULL, fit);
+      const int ffit = mfit ? __ffs(mfit) - 1 : 32;
+      int act = ffit;
+      if (can_preempt && ffit > 0) {
+        if (V < 0) {
+          V = build_victims();
+          vr = lane < V ? p.v_rem[lane] : -1;
+          vc = lane < V ? p.v_cum[lane] : 0;
         }
-        if (ok) { best = key; best_k = k; }
+        // G(rem) = blocks of eligible victims with remaining > rem: non-increasing in rem, and the
+        // chunk's candidates are in ascending rem, so G(first candidate) bounds the whole chunk
+        const int rem0 = __shfl_sync(FULL, rem, 0);
+        long long g0;
+        if (V <= 32) {
+          const int m0 = __popc(__ballot_sync(FULL, vr > rem0));
+          g0 = m0 > 0 ? __shfl_sync(FULL, vc, m0 - 1) : 0;
+        } else {
+          const int m0 = victims_above(V, rem0);
+          g0 = m0 > 0 ? p.v_cum[m0 - 1] : 0;
+        }
+        const bool maybe = v && !fit && lane < ffit && (long long)need <= (long long)free + g0;
+        if (__any_sync(FULL, maybe)) {
+          long long gain;
+          if (V <= 32) {
+            int m = 0;
+            for (int u = 0; u < V; ++u) m += __shfl_sync(FULL, vr, u) > rem;
+            gain = __shfl_sync(FULL, vc, m > 0 ? m - 1 : 0);
+            if (m == 0) gain = 0;
+          } else {
+            const int m = maybe ? victims_above(V, rem) : 0;
+            gain = m > 0 ? p.v_cum[m - 1] : 0;
+          }
+          const unsigned mcov = __ballot_sync(FULL, maybe && (long long)free + gain >= need);
+          if (mcov) act = __ffs(mcov) - 1;
+        }
       }
-      unsigned win = warp_argmin_u64(best, best != ~0ULL);  // keys are unique
-      if (win == 0u) break;
-      best = __shfl_sync(FULL, best, __ffs(win) - 1);
-      best_k = __shfl_sync(FULL, best_k, __ffs(win) - 1);
-      int pos = phys(best_k);
-      int need = blocks(p.w_pend[pos]);
-      int rem = (int)(best >> 32);
-      if (need > free) {
+      if (act == 32) { k0 += 32; continue; }
+      const int cpos = k0 + act;
+      const int crem = __shfl_sync(FULL, rem, act);
+      const int cpend = __shfl_sync(FULL, pend, act);
+      const int cneed = blocks(cpend);
+      const int rid_flag = p.w_rid[cpos];
+      if (cneed > free) {
         // take victims (largest remaining first, youngest first on ties) until free+gain >= need
-        int m = victims_above(V, rem);
+        const int m = victims_above(V, crem);
         long long gain = 0;
         int taken = 0;
-        while (taken < m && (long long)free + gain < need) {
+        while (taken < m && (long long)free + gain < cneed) {
           gain = p.v_cum[taken];
           taken++;
         }
         for (int t = lane; t < taken; t += 32) {
-          int j = p.v_idx[t];
+          const int j = p.v_idx[t];
           p.r_plan[j] = 1;  // marked
           p.l_b[np + t] = j;
         }
         np += taken;
         free += (int)gain;
-        V = -1;  // marks changed: rebuild before the next candidate
+        V = -1;  // marks changed: rebuild before the next coverability check
         __syncwarp();
       }
-      if (lane == 0) p.l_a[nd] = pos;
+      if (lane == 0) { p.l_a[nd] = rid_flag; p.l_c[nd] = cpend; }
       nd++;
-      free -= need;
-      last = best;
+      free -= cneed;
+      __syncwarp();
+      trail_remove(cpos);  // the next candidate moves into slot cpos
+      k0 = cpos;
     }
     __syncwarp();
     nd_out = nd;
@@ -631,10 +739,11 @@ struct Eng {
       bool valid = j < nd;
       int rid = 0;
       if (valid) {
+        const bool listed = cfg.policy == SSB_POLICY_TRAIL_PLUS;
         int pos = prefix_mode ? phys(j) : p.l_a[j];
-        int wr = p.w_rid[pos];
+        int wr = listed ? p.l_a[j] : p.w_rid[pos];
         rid = wr & 0x7fffffff;
-        int pend = p.w_pend[pos];
+        int pend = listed ? p.l_c[j] : p.w_pend[pos];
         int pr = prompt[rid];
         int t = st.R + j;
         p.r_rid[t] = rid;
@@ -646,7 +755,7 @@ struct Eng {
         if (!(wr & FLAG_SEEN)) rec_fd[rid] = st.clock;  // first dispatch (queueing delay)
         need_sum += blocks(pend);
         pend_sum += pend;
-        if (cfg.policy == SSB_POLICY_NOPREEMPT) res_sum += p.w_key[pos];
+        if (cfg.policy == SSB_POLICY_NOPREEMPT) res_sum += p.w_key[pos];  // (listed mode: trail_plus only)
       }
       emit(__ballot_sync(FULL, valid), SSB_EV_DISPATCH, rid);
     }
@@ -664,7 +773,7 @@ struct Eng {
     if (prefix_mode) {
       st.whead = phys(nd);
       st.W -= nd;
-    } else {
+    } else if (cfg.policy != SSB_POLICY_TRAIL_PLUS) {  // trail_plus removed them during select
       remove_dispatched_unordered(nd);
     }
   }

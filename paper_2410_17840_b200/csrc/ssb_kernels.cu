@@ -26,7 +26,7 @@ __host__ __device__ inline long long align_up(long long x, long long a) { return
 
 struct Layout {
   long long srv, w_enq, w_rid, w_pend, w_key, r_rid, r_prompt, r_out, r_gen, r_pfd, r_st, r_plan, l_a, l_b, v_idx,
-      v_rem, v_cum, rl, total;
+      v_rem, v_cum, v_key, l_c, rl, total;
 };
 
 __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers) {
@@ -49,6 +49,8 @@ __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long l
   L.v_idx = o;    o = align_up(o + 4 * Rc, 64);
   L.v_rem = o;    o = align_up(o + 4 * Rc, 64);
   L.v_cum = o;    o = align_up(o + 8 * Rc, 64);
+  L.v_key = o;    o = align_up(o + 8 * Rc, 64);
+  L.l_c = o;      o = align_up(o + 4 * Rc, 64);
   L.rl = o;       o = align_up(o + (n_servers > 1 ? 4 * N : 0), 64);
   L.total = align_up(o, 256);
   return L;
@@ -72,6 +74,8 @@ __device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
   p.v_idx = (int*)(base + L.v_idx);
   p.v_rem = (int*)(base + L.v_rem);
   p.v_cum = (long long*)(base + L.v_cum);
+  p.v_key = (unsigned long long*)(base + L.v_key);
+  p.l_c = (int*)(base + L.l_c);
   p.rl = (int*)(base + L.rl);
   return p;
 }
@@ -109,7 +113,9 @@ __device__ inline void init_srv(Srv& s, const Cfg& c) {
   s.R = s.W = s.whead = s.committed = s.next_arr = s.status = s.ndec = 0;
 }
 
-constexpr int SM_COLS = 9;  // r_rid r_prompt r_out r_gen r_pfd r_st r_plan l_a l_b
+// shared running table columns: r_rid r_prompt r_out r_gen r_pfd r_st r_plan l_a l_b
+// v_idx v_rem v_cum(2) v_key(2) l_c
+constexpr int SM_COLS = 16;
 constexpr int RS = SSB_SMEM_RUN_CAP;
 
 // sm_tab: this engine's shared-memory running table (SM_COLS x RS ints) or
@@ -129,6 +135,11 @@ __device__ inline void bind_engine(Eng& E, const ssb_instance& I, const Cfg& cfg
     E.p.r_plan = sm_tab + 6 * RS;
     E.p.l_a = sm_tab + 7 * RS;
     E.p.l_b = sm_tab + 8 * RS;
+    E.p.v_idx = sm_tab + 9 * RS;
+    E.p.v_rem = sm_tab + 10 * RS;
+    E.p.v_cum = (long long*)(sm_tab + 11 * RS);
+    E.p.v_key = (unsigned long long*)(sm_tab + 13 * RS);
+    E.p.l_c = sm_tab + 15 * RS;
     if (E.cfg.Rc > RS) E.cfg.Rc = RS;  // overflow -> SSB_E_CAPACITY -> host re-runs with global tables
   }
   E.arrival = tr.arrival + I.trace_offset;
@@ -278,7 +289,7 @@ struct ClusterShared {
 };
 
 constexpr int CLUSTER_MAX_WARPS = 8;
-constexpr int CLUSTER_SMEM_SERVERS = 16;  // 16 x 9 KiB shared running tables
+constexpr int CLUSTER_SMEM_SERVERS = 12;  // 12 x 15 KiB shared running tables
 
 __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr,
                           ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch,
