@@ -52,6 +52,8 @@ def config(world: int) -> dict:
         "parallelism": f"instance-sharded x{world}" + (" + NCCL all_gather of summaries" if world > 1 else ""),
         "l2": "working set (trace+records+scratch, ~1 GB per GPU) exceeds L2; L2 flushed (256 MB write) before "
               "every timed step",
+        "schedule": "per-policy persistent kernels sharing the GPU by estimated work, longest-first queues; "
+                    "estimates = device cycles of each instance measured in the untimed first pass",
     }
 
 
@@ -213,6 +215,7 @@ def main() -> None:
     stats, _ = runner.results()
     overflow_reruns = runner.fix_overflows()
     stats, summaries = runner.results()
+    runner.adopt_measured_schedule(stats)  # placement hint for the next runs
     if (stats["status"] != 0).any():
         raise SystemExit(f"rank {rank}: instance status {np.unique(stats['status'])}")
     rsteps = int(stats["request_steps"].sum())

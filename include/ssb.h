@@ -131,6 +131,8 @@ typedef struct {
   uint64_t digest;         /* FNV-1a fold of per-engine event digests  */
   int32_t status;          /* SSB_OK or SSB_E_*                                           */
   int32_t _pad;
+  int64_t device_cycles;   /* SM clock cycles the instance took (scheduling feedback: feed
+                              back as ssb_instance.est_cost to order the next launch)     */
 } ssb_stats;
 
 /* Optional event log (engine.py:267-274) */

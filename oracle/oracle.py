@@ -35,7 +35,8 @@ _lib = None
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < (ORACLE_DIR / "ssb_oracle.c").stat().st_mtime:
+    deps = [ORACLE_DIR / "ssb_oracle.c", ROOT / "include" / "ssb.h"]
+    if force or not LIB.exists() or any(LIB.stat().st_mtime < d.stat().st_mtime for d in deps):
         subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "-B" if force else "libssb_oracle.so"], check=True)
     return LIB
 

@@ -79,6 +79,7 @@ STATS = np.dtype(
         ("digest", "<u8"),
         ("status", "<i4"),
         ("_pad", "<i4"),
+        ("device_cycles", "<i8"),
     ],
     align=True,
 )
@@ -199,7 +200,7 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path is not None else LIB_PATH
+    p = Path(path) if path is not None else Path(os.environ.get("SSB_LIB", LIB_PATH))
     if not p.exists():
         raise NativeLibraryMissing(
             f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -40,7 +40,7 @@ constexpr unsigned long long FNV_PRIME = 0x100000001b3ULL;
 
 struct Cfg {
   int policy, max_output, bs, bs_shift, pool, cap, max_running, max_ctx;
-  int n_servers, Wc, Rc;
+  int n_servers, Wc, Rc, NB;
   double alpha, c, mem_base, mem_kv, compute, overhead, qps;
 };
 
@@ -55,6 +55,7 @@ struct Srv {
   long long ev_n;
   long long pf_pend;         // Σ pending over PREFILLING entries
   int free_blocks, R, W, whead, committed, next_arr, status, ndec;
+  int nbl, nfree, nalloc;    // trail_plus blocked waiting list: blocks in list / free stack / bump
 };
 
 struct SrvPtr {
@@ -72,6 +73,16 @@ struct SrvPtr {
   int* l_a;   // dispatch list (physical ring slots) / scratch list
   int* l_b;   // preempt list (table indices) / scratch list
   int* l_c;   // trail_plus dispatch list: pending prefill
+  // trail_plus waiting set: ordered list of 32-slot blocks, each sorted by key
+  unsigned long long* bk_key;  // [NB*32] remaining<<32 | id
+  int* bk_rid;                 // [NB*32] id | FLAG_SEEN
+  int* bk_pend;                // [NB*32] pending prefill
+  int* bm_cnt;                 // [NB] entries in the block
+  int* bm_min;                 // [NB] min block need in the block
+  unsigned long long* bm_first;  // [NB] first / last key
+  unsigned long long* bm_last;
+  int* b_list;                 // [NB] block ids in key order
+  int* b_free;                 // [NB] free-block stack
   int* v_idx; // trail_plus victims sorted by (-remaining, -dispatch_seq)
   int* v_rem;
   long long* v_cum;
@@ -137,6 +148,71 @@ __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool
 // the integer division would otherwise be inlined at every call site)
 __device__ __noinline__ int div_up_slow(int t, int bs) { return (t + bs - 1) / bs; }
 
+// FNV-1a over the 64-bit words (code, request id, time bits) of one event
+__device__ __noinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
+  h ^= (unsigned long long)code; h *= FNV_PRIME;
+  h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
+  h ^= (unsigned long long)__double_as_longlong(t); h *= FNV_PRIME;
+  return h;
+}
+__device__ __noinline__ void write_event(ssb_event* ev, long long pos, long long cap, double t, int rid, int server,
+                                         int code) {
+  if (pos < cap) {
+    ssb_event e;
+    e.time = t;
+    e.request_id = rid;
+    e.server = (int16_t)server;
+    e.code = (int16_t)code;
+    ev[pos] = e;
+  }
+}
+
+// Warp bitonic sort, descending, of 32*K 64-bit keys held in registers: element i = k*32 + lane.
+// Pad unused elements with 0 (they sort last).
+template <int K>
+__device__ __forceinline__ void warp_sort_desc(unsigned long long (&x)[K], int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32 * K; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int i = k * 32 + lane;
+        const bool desc = (i & size) == 0;  // this size-block is sorted descending
+        if (stride >= 32) {
+          const int kj = k ^ (stride >> 5);
+          if (kj > k) {
+            const unsigned long long a = x[k], b = x[kj];
+            const bool sw = desc ? (a < b) : (a > b);
+            x[k] = sw ? b : a;
+            x[kj] = sw ? a : b;
+          }
+        } else {
+          const unsigned long long o = __shfl_xor_sync(FULL, x[k], stride);
+          const bool lower = (i & stride) == 0;
+          const bool keep_max = lower == desc;
+          x[k] = keep_max ? (x[k] > o ? x[k] : o) : (x[k] < o ? x[k] : o);
+        }
+      }
+    }
+  }
+}
+
+// Sort keys[0..n) (n <= 256) descending in place: 8 registers per lane, one bitonic network.
+// Out of line: one copy of the network in the image, register-only interface.
+__device__ __noinline__ void sort_keys_desc_256(unsigned long long* keys, int n) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = (k * 32 + lane < n) ? keys[k * 32 + lane] : 0ULL;
+  warp_sort_desc<8>(x, lane);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (k * 32 + lane < n) keys[k * 32 + lane] = x[k];
+  __syncwarp();
+}
+
 // stable compaction of a running table (drops ST_GONE entries); returns the new size.
 // Out of line with pointer/int arguments only, so callers keep their state in registers.
 __device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restrict__ r_prompt, int* __restrict__ r_out,
@@ -164,7 +240,18 @@ __device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restri
   return out;
 }
 
+#ifdef SSB_PHASE_TIMING
+#define SSB_T0(name) long long _t_##name = clock64();
+#define SSB_T1(name, slot) tm[slot] += clock64() - _t_##name; tc[slot] += 1;
+#else
+#define SSB_T0(name)
+#define SSB_T1(name, slot)
+#endif
+
 struct Eng {
+#ifdef SSB_PHASE_TIMING
+  long long tm[8], tc[8];  // 0 enqueue 1 select 2 preempt+dispatch 3 fast 4 small 5 general 6/7 walk counters
+#endif
   Cfg cfg;
   Srv st;
   SrvPtr p;
@@ -190,8 +277,21 @@ struct Eng {
   // dispatch nothing: FCFS & NoPreempt (free only shrinks, committed fixed),
   // trail_plus (free + coverable victim blocks never grows), any policy with W == 0.
   bool nodisp;
+  // larry top cache: the last full scan's winner (physical slot, pending) and the margin
+  // delta >= (exact score gap to every other candidate) that certifies it stays the
+  // winner while the waiting set (and so queue_len) is unchanged: see select_larry
+  bool lc_valid;
+  int lc_pos, lc_pend;
+  double lc_delta, lc_emin;
+  long long lc_pmax;
 
-  __device__ __forceinline__ void init_modes() { regs_ok = regs_dirty = false; rsum = 0; nodisp = false; }
+  __device__ __forceinline__ void init_modes() {
+    regs_ok = regs_dirty = false;
+    rsum = 0;
+    nodisp = false;
+    lc_valid = false;
+    nq = 0;
+  }
   __device__ __forceinline__ void flush_regs() {
     if (regs_dirty) {
       if (lane < st.R) p.r_gen[lane] = c_g0;
@@ -236,23 +336,9 @@ struct Eng {
   __device__ __forceinline__ bool has_work() const { return st.W > 0 || st.R > 0; }
 
   // ---- event log + decision digest (engine.py:273-274) ----
-  __device__ __forceinline__ void fold(int code, int rid) {
-    unsigned long long tb = (unsigned long long)__double_as_longlong(st.clock);
-    unsigned long long h = st.digest;
-    h ^= (unsigned long long)code; h *= FNV_PRIME;
-    h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
-    h ^= tb; h *= FNV_PRIME;
-    st.digest = h;
-  }
+  __device__ __forceinline__ void fold(int code, int rid) { st.digest = fnv_event(st.digest, code, rid, st.clock); }
   __device__ __forceinline__ void log_at(long long pos, int code, int rid) {
-    if (ev != nullptr && pos < ev_cap) {
-      ssb_event e;
-      e.time = st.clock;
-      e.request_id = rid;
-      e.server = (int16_t)server;
-      e.code = (int16_t)code;
-      ev[pos] = e;
-    }
+    if (ev != nullptr) write_event(ev, pos, ev_cap, st.clock, rid, server, code);
   }
   // one event per lane in `mask`, lane order (warp-uniform call)
   __device__ void emit(unsigned mask, int code, int rid_lane) {
@@ -290,56 +376,145 @@ struct Eng {
     st.ev_n += 1;
   }
 
-  // ---- trail_plus waiting set: slots [0, W) sorted by key = (remaining << 32 | id) ----
-  // (whead stays 0; the 64-bit key lives in the w_enq column, rid|flag in w_rid, pending in w_pend)
-  __device__ __forceinline__ unsigned long long* wkey64() const { return reinterpret_cast<unsigned long long*>(p.w_enq); }
-  __device__ int trail_lower_bound(unsigned long long k, int n) const {  // first slot with key >= k
-    int lo = 0, hi = n;
-    while (hi - lo > 32) {  // 32-ary search: one ballot per level
-      const int step = (hi - lo + 31) >> 5;
-      const int pos = lo + lane * step;
-      const unsigned m = __ballot_sync(FULL, pos < hi && wkey64()[pos] < k);
-      const int c = __popc(m);
-      const int nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
-      const int nhi = min(hi, lo + c * step);
-      lo = nlo;
-      hi = nhi;
+  // ---- trail_plus waiting set: an ordered list of 32-slot blocks, sorted by key =
+  // (remaining << 32 | id). Insert / remove touch one block (one warp chunk: shuffles);
+  // a full block splits in two, a block under 8 entries merges with its successor when
+  // they fit; per-block (count, min need, first, last key) let the walk skip blocks. ----
+  __device__ __forceinline__ int blk_alloc() {
+    if (st.nfree > 0) return p.b_free[--st.nfree];
+    if (st.nalloc < cfg.NB) return st.nalloc++;
+    st.status = SSB_E_CAPACITY;
+    return 0;
+  }
+  __device__ __forceinline__ void blk_meta(int b, int cnt, unsigned long long key, int pend) {
+    const unsigned mn = __reduce_min_sync(FULL, lane < cnt ? (unsigned)blocks(pend) : 0x7fffffffu);
+    const unsigned long long first = __shfl_sync(FULL, key, 0), last = __shfl_sync(FULL, key, (cnt - 1) & 31);
+    if (lane == 0) { p.bm_cnt[b] = cnt; p.bm_min[b] = (int)mn; p.bm_first[b] = first; p.bm_last[b] = last; }
+  }
+  __device__ __forceinline__ void blk_load(int b, int cnt, unsigned long long& key, int& rid, int& pend) const {
+    key = ~0ULL; rid = 0; pend = 0;
+    if (lane < cnt) { const int s = b * 32 + lane; key = p.bk_key[s]; rid = p.bk_rid[s]; pend = p.bk_pend[s]; }
+  }
+  __device__ __forceinline__ void blk_store(int b, int lo, int hi, unsigned long long key, int rid, int pend) {
+    if (lane >= lo && lane < hi) { const int s = b * 32 + lane; p.bk_key[s] = key; p.bk_rid[s] = rid; p.bk_pend[s] = pend; }
+  }
+  __device__ int blk_find(unsigned long long k) const {  // first block whose last key >= k, else the last
+    for (int base = 0; base < st.nbl; base += 32) {
+      const int i = base + lane;
+      const unsigned m = __ballot_sync(FULL, i < st.nbl && p.bm_last[p.b_list[i]] >= k);
+      if (m) return base + __ffs(m) - 1;
     }
-    const int pos = lo + lane;
-    return lo + __popc(__ballot_sync(FULL, pos < hi && wkey64()[pos] < k));
+    return st.nbl - 1;
+  }
+  __device__ void list_insert(int at, int nb) {
+    for (int hi = st.nbl; hi > at; hi -= 32) {
+      const int i = max(at, hi - 32) + lane;
+      const int x = i < hi ? p.b_list[i] : 0;
+      __syncwarp();
+      if (i < hi) p.b_list[i + 1] = x;
+      __syncwarp();
+    }
+    if (lane == 0) p.b_list[at] = nb;
+    __syncwarp();
+    st.nbl += 1;
+  }
+  __device__ void list_remove(int at) {
+    for (int lo = at + 1; lo < st.nbl; lo += 32) {
+      const int i = lo + lane;
+      const int x = i < st.nbl ? p.b_list[i] : 0;
+      __syncwarp();
+      if (i < st.nbl) p.b_list[i - 1] = x;
+      __syncwarp();
+    }
+    st.nbl -= 1;
+  }
+  __device__ __forceinline__ void blk_release(int b) {
+    if (lane == 0) p.b_free[st.nfree] = b;
+    __syncwarp();
+    st.nfree += 1;
   }
   __device__ void trail_insert(int rid_flag, int pend, int rem) {
     const unsigned long long k = ((unsigned long long)(unsigned)rem << 32) | (unsigned)(rid_flag & 0x7fffffff);
-    const int n = st.W;
-    if (n + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
-    const int pos = trail_lower_bound(k, n);
-    for (int hi = n; hi > pos; hi -= 32) {  // shift [pos, n) up one slot, top chunk first
-      const int lo = max(pos, hi - 32);
-      const int i = lo + lane;
-      const bool v = i < hi;
-      unsigned long long kk = 0;
-      int r = 0, pd = 0;
-      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
+    if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
+    if (st.nbl == 0) {
+      const int b = blk_alloc();
+      if (st.status) return;
+      if (lane == 0) p.bm_cnt[b] = 0;
       __syncwarp();
-      if (v) { wkey64()[i + 1] = kk; p.w_rid[i + 1] = r; p.w_pend[i + 1] = pd; }
-      __syncwarp();
+      list_insert(0, b);
     }
-    if (lane == 0) { wkey64()[pos] = k; p.w_rid[pos] = rid_flag; p.w_pend[pos] = pend; }
+    int bi = blk_find(k);
+    int b = p.b_list[bi];
+    int cnt = p.bm_cnt[b];
+    unsigned long long key;
+    int rid, pd;
+    blk_load(b, cnt, key, rid, pd);
+    if (cnt == 32) {  // split: the upper half moves to a new block after b
+      const int nb = blk_alloc();
+      if (st.status) return;
+      const unsigned long long ukey = __shfl_down_sync(FULL, key, 16);
+      const int urid = __shfl_down_sync(FULL, rid, 16), upd = __shfl_down_sync(FULL, pd, 16);
+      blk_store(nb, 0, 16, ukey, urid, upd);
+      blk_meta(nb, 16, ukey, upd);
+      blk_meta(b, 16, key, pd);
+      __syncwarp();
+      list_insert(bi + 1, nb);
+      const unsigned long long last_lo = __shfl_sync(FULL, key, 15);
+      cnt = 16;
+      if (k > last_lo) { bi += 1; b = nb; key = ukey; rid = urid; pd = upd; }
+      if (lane >= 16) { key = ~0ULL; rid = 0; pd = 0; }
+    }
+    const int pos = __popc(__ballot_sync(FULL, lane < cnt && key < k));
+    const unsigned long long nk = __shfl_up_sync(FULL, key, 1);
+    const int nr = __shfl_up_sync(FULL, rid, 1), np = __shfl_up_sync(FULL, pd, 1);
+    if (lane > pos) { key = nk; rid = nr; pd = np; }
+    if (lane == pos) { key = k; rid = rid_flag; pd = pend; }
+    cnt += 1;
+    blk_store(b, pos, cnt, key, rid, pd);
+    blk_meta(b, cnt, key, pd);
     __syncwarp();
-    st.W = n + 1;
+    st.W += 1;
   }
-  __device__ void trail_remove(int pos) {  // shift (pos, W) down one slot
-    for (int lo = pos + 1; lo < st.W; lo += 32) {
-      const int i = lo + lane;
-      const bool v = i < st.W;
-      unsigned long long kk = 0;
-      int r = 0, pd = 0;
-      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
-      __syncwarp();
-      if (v) { wkey64()[i - 1] = kk; p.w_rid[i - 1] = r; p.w_pend[i - 1] = pd; }
-      __syncwarp();
-    }
+  // remove slot `pos` of the block at list index bi
+  __device__ void trail_remove_at(int bi, int pos) {
+    const int b = p.b_list[bi];
+    int cnt = p.bm_cnt[b];
+    unsigned long long key;
+    int rid, pd;
+    blk_load(b, cnt, key, rid, pd);
+    const unsigned long long nk = __shfl_down_sync(FULL, key, 1);
+    const int nr = __shfl_down_sync(FULL, rid, 1), np = __shfl_down_sync(FULL, pd, 1);
+    if (lane >= pos) { key = nk; rid = nr; pd = np; }
+    cnt -= 1;
     st.W -= 1;
+    if (cnt == 0) {
+      list_remove(bi);
+      blk_release(b);
+      return;
+    }
+    if (lane >= cnt) { key = ~0ULL; rid = 0; pd = 0; }
+    blk_store(b, pos, cnt, key, rid, pd);
+    if (cnt < 8 && bi + 1 < st.nbl) {  // merge the successor in when both fit
+      const int nb = p.b_list[bi + 1];
+      const int ncnt = p.bm_cnt[nb];
+      if (cnt + ncnt <= 32) {
+        unsigned long long k2;
+        int r2, p2;
+        blk_load(nb, ncnt, k2, r2, p2);
+        const unsigned long long mk = __shfl_up_sync(FULL, k2, cnt);
+        const int mr = __shfl_up_sync(FULL, r2, cnt), mp = __shfl_up_sync(FULL, p2, cnt);
+        if (lane >= cnt && lane < cnt + ncnt) { key = mk; rid = mr; pd = mp; }
+        blk_store(b, cnt, cnt + ncnt, key, rid, pd);
+        cnt += ncnt;
+        blk_meta(b, cnt, key, pd);
+        __syncwarp();
+        list_remove(bi + 1);
+        blk_release(nb);
+        return;
+      }
+    }
+    blk_meta(b, cnt, key, pd);
+    __syncwarp();
   }
 
   // ---- Engine.enqueue for every routed arrival with arrival <= clock (engine.py:175-184, 261-262) ----
@@ -379,6 +554,7 @@ struct Eng {
       }
       emit(m, SSB_EV_ENQUEUE, rid);
       nodisp = false;
+      lc_valid = false;
       long long s = warp_sum_ll(pr);
       if (!trail) st.W += cnt;
       st.wpend_sum += s;
@@ -390,35 +566,50 @@ struct Eng {
   }
 
   // ---- push a running entry back to the waiting head (_preempt, engine.py:368-379) ----
-  // uniform call; the entry is table index j with loaded fields
+  // uniform call; the entry is table index j with loaded fields. Accounting, the table mark
+  // and the event happen now; the waiting-set insertion is queued (v_* columns, free outside
+  // select) and done by flush_pushes() in the same order, before anything reads the queue.
+  int nq;  // queued waiting pushes
   __device__ void preempt_entry(int j, int rid, int pr, int out, int gen, int pfd, int state, int code) {
     nodisp = false;
+    lc_valid = false;
     int alloc = pr + gen;  // KV tokens held
     st.free_blocks += blocks(alloc);
     if (state == ST_DECODE) st.ndec -= 1;
     else st.pf_pend -= (long long)(alloc - pfd);
     if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= wkey_for(pr, out, gen);
-    if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
-    if (cfg.policy == SSB_POLICY_TRAIL_PLUS) {  // sorted waiting set: order is by key, not by deque position
-      if (lane == 0) { p.r_st[j] = ST_GONE; rec_pc[rid] += 1; }
-      __syncwarp();
-      trail_insert(rid | FLAG_SEEN, alloc, out - gen);
-    } else {
-      st.whead = (st.whead == 0) ? cfg.Wc - 1 : st.whead - 1;
-      if (lane == 0) {
-        int pos = st.whead;
-        p.w_rid[pos] = rid | FLAG_SEEN;
-        p.w_pend[pos] = alloc;  // pending_prefill = prompt + generated (prefill_done reset)
-        p.w_key[pos] = wkey_for(pr, out, gen);
-        p.w_enq[pos] = st.clock;
-        p.r_st[j] = ST_GONE;
-        rec_pc[rid] += 1;
-      }
-      st.W += 1;
+    if (lane == 0) {
+      p.r_st[j] = ST_GONE;
+      rec_pc[rid] += 1;
+      p.v_idx[nq] = rid | FLAG_SEEN;
+      p.v_rem[nq] = alloc;  // pending_prefill = prompt + generated (prefill_done reset)
+      p.v_cum[nq] = wkey_for(pr, out, gen);
     }
+    nq += 1;
     st.wpend_sum += alloc;
     if (code == SSB_EV_PARK) st.parks += 1; else st.preempts += 1;
     emit1(code, rid);
+    __syncwarp();
+  }
+  __device__ void flush_pushes() {
+    for (int i = 0; i < nq; ++i) {
+      const int rid_flag = p.v_idx[i], alloc = p.v_rem[i], key = (int)p.v_cum[i];
+      if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; break; }
+      if (cfg.policy == SSB_POLICY_TRAIL_PLUS) {  // sorted waiting set: order is by key, not by deque position
+        trail_insert(rid_flag, alloc, key);
+      } else {
+        st.whead = (st.whead == 0) ? cfg.Wc - 1 : st.whead - 1;
+        if (lane == 0) {
+          const int pos = st.whead;
+          p.w_rid[pos] = rid_flag;
+          p.w_pend[pos] = alloc;
+          p.w_key[pos] = key;
+          p.w_enq[pos] = st.clock;
+        }
+        st.W += 1;
+      }
+    }
+    nq = 0;
     __syncwarp();
   }
 
@@ -458,6 +649,30 @@ struct Eng {
   }
 
   // ---- LARRY (policies.py:244-276): ordered extraction by (-score, enqueue_time, id) ----
+  // One scan of the waiting ring yields the top two candidates (each lane keeps its best
+  // two, the warp takes the argmax, then the argmax of the runner-ups), so a step that
+  // dispatches at most one request never rescans.
+  struct LKey {
+    double sc, enq;
+    int rid, k;
+  };
+  __device__ __forceinline__ static bool lbetter(const LKey& x, const LKey& y) {  // x before y in the order
+    return x.sc > y.sc || (x.sc == y.sc && (x.enq < y.enq || (x.enq == y.enq && x.rid < y.rid)));
+  }
+  __device__ __forceinline__ unsigned larry_argmax(const LKey& x, bool has) const {
+    unsigned win = warp_argmax_u64(dkey(x.sc), has);
+    if (win & (win - 1)) win = warp_argmax_u64(~dkey(x.enq), has && ((win >> lane) & 1u));
+    if (win & (win - 1)) win = warp_argmax_u64(~(unsigned long long)(unsigned)x.rid, has && ((win >> lane) & 1u));
+    return win;
+  }
+  __device__ __forceinline__ LKey lshfl(const LKey& x, int src) const {
+    LKey y;
+    y.sc = __shfl_sync(FULL, x.sc, src);
+    y.enq = __shfl_sync(FULL, x.enq, src);
+    y.rid = __shfl_sync(FULL, x.rid, src);
+    y.k = __shfl_sync(FULL, x.k, src);
+    return y;
+  }
   __device__ int select_larry() {
     if (st.W == 0) return 0;
     long long slots = cfg.max_running < 0 ? (1LL << 40) : (long long)cfg.max_running - st.R;
@@ -468,50 +683,105 @@ struct Eng {
     if (budget < 0) budget = 0;
     int free = st.free_blocks;
     const long long ql = st.W;  // queue_len, fixed for the step (:259)
+    if (slots <= 0 || budget <= 0 || free <= 0) return 0;
+    if (lc_valid) {
+      // Scores are fl(fl(a*fl(clock-enq)) - ql*pending): in exact arithmetic every score moves by
+      // the same a*dclock, so exact gaps are constant; each computed score is within
+      // E = (3*a*(clock-enq) + ql*pending) * 2^-53 (x1.0001) of its exact value. If the cached
+      // winner led every other candidate by delta (exact gap lower bound) and delta > 2E(clock),
+      // it is still the strict winner; if it does not fit, nothing is dispatched this step.
+      const double E = (3.0 * cfg.alpha * (st.clock - lc_emin) + (double)(ql * lc_pmax)) * 1.1102230246251565e-16 * 1.0001;
+      if (lc_delta > 2.0 * E) {
+        if (blocks(lc_pend) > free) return 0;
+      }
+      lc_valid = false;  // (it fits, or the margin is too thin: rescan)
+    }
     int nd = 0;
     bool have_last = false;
-    double l_sc = 0.0, l_enq = 0.0;
-    int l_rid = 0;
+    bool first_scan = true;
+    LKey last{0.0, 0.0, 0, -1};
     while (true) {
       if ((long long)nd >= slots || budget <= 0 || free <= 0) break;  // need >= 1 always
-      bool found = false;
-      double b_sc = 0.0, b_enq = 0.0;
-      int b_rid = 0x7fffffff, b_k = -1;
-      for (int k = lane; k < st.W; k += 32) {
-        int pos = phys(k);
-        int rid = p.w_rid[pos] & 0x7fffffff;
-        int pend = p.w_pend[pos];
-        double enq = p.w_enq[pos];
-        // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending
-        double sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, enq)), (double)(ql * (long long)pend));
-        if (have_last) {  // strictly after the last extracted key
-          bool after = (sc < l_sc) || (sc == l_sc && (enq > l_enq || (enq == l_enq && rid > l_rid)));
-          if (!after) continue;
+      bool h1 = false, h2 = false;
+      LKey b1{0.0, 0.0, 0x7fffffff, -1}, b2{0.0, 0.0, 0x7fffffff, -1};
+      for (int k0 = 0; k0 < st.W; k0 += 64) {  // two independent elements per lane per trip
+        LKey x[2];
+        bool hx[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = k0 + 32 * u + lane;
+          hx[u] = k < st.W;
+          if (hx[u]) {
+            const int pos = phys(k);
+            x[u].rid = p.w_rid[pos] & 0x7fffffff;
+            x[u].enq = p.w_enq[pos];
+            x[u].k = k;
+            const int pend = p.w_pend[pos];
+            // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending
+            x[u].sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, x[u].enq)), (double)(ql * (long long)pend));
+          }
         }
-        bool better = !found || (sc > b_sc) || (sc == b_sc && (enq < b_enq || (enq == b_enq && rid < b_rid)));
-        if (better) { found = true; b_sc = sc; b_enq = enq; b_rid = rid; b_k = k; }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!hx[u] || (have_last && !lbetter(last, x[u]))) continue;  // only keys strictly after `last`
+          if (!h1 || lbetter(x[u], b1)) { b2 = b1; h2 = h1; b1 = x[u]; h1 = true; }
+          else if (!h2 || lbetter(x[u], b2)) { b2 = x[u]; h2 = true; }
+        }
       }
-      // warp argmax of (score, -enqueue_time, -id): REDUX on orderable keys, ties rare
-      unsigned win = warp_argmax_u64(dkey(b_sc), found);
-      if (win == 0u) break;
-      if (win & (win - 1)) win = warp_argmax_u64(~dkey(b_enq), found && ((win >> lane) & 1u));
-      if (win & (win - 1)) win = warp_argmax_u64(~(unsigned long long)(unsigned)b_rid, found && ((win >> lane) & 1u));
-      const int wl = __ffs(win) - 1;
-      b_sc = __shfl_sync(FULL, b_sc, wl);
-      b_enq = __shfl_sync(FULL, b_enq, wl);
-      b_rid = __shfl_sync(FULL, b_rid, wl);
-      b_k = __shfl_sync(FULL, b_k, wl);
-      found = true;
-      if (!found) break;
-      int pos = phys(b_k);
-      int pend = p.w_pend[pos];
-      int need = blocks(pend);
-      if (need > free) break;
-      if (lane == 0) p.l_a[nd] = pos;
-      nd++;
-      free -= need;
-      budget -= min((long long)pend, budget);
-      have_last = true; l_sc = b_sc; l_enq = b_enq; l_rid = b_rid;
+      const unsigned w1 = larry_argmax(b1, h1);
+      if (w1 == 0u) break;
+      const int wl = __ffs(w1) - 1;
+      const LKey top = lshfl(b1, wl);
+      // runner-up: the winner lane offers its second best, every other lane its best
+      const bool hr = (lane == wl) ? h2 : h1;
+      const LKey rc = (lane == wl) ? b2 : b1;
+      const unsigned w2 = larry_argmax(rc, hr);
+      if (first_scan) {
+        first_scan = false;
+        // certify the winner for later steps: exact gap to any other candidate >= delta
+        double emin = 1e300;
+        long long pmax = 0;
+        for (int k = lane; k < st.W; k += 32) {
+          const int pos = phys(k);
+          emin = fmin(emin, p.w_enq[pos]);
+          pmax = max(pmax, (long long)p.w_pend[pos]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          emin = fmin(emin, __shfl_xor_sync(FULL, emin, o));
+          pmax = max(pmax, __shfl_xor_sync(FULL, pmax, o));
+        }
+        const double E0 = (3.0 * cfg.alpha * (st.clock - emin) + (double)(ql * pmax)) * 1.1102230246251565e-16 * 1.0001;
+        const double sc2 = w2 ? __shfl_sync(FULL, rc.sc, __ffs(w2) - 1) : -1e300;
+        lc_delta = w2 ? (top.sc - sc2) - 2.0 * E0 : 1e300;  // a single candidate leads by infinity
+        lc_emin = emin;
+        lc_pmax = pmax;
+        lc_pos = phys(top.k);
+        lc_pend = p.w_pend[lc_pos];
+        lc_valid = true;  // cleared by any dispatch / enqueue / preemption
+      }
+      int taken = 0;
+      for (int t = 0; t < 2; ++t) {
+        LKey c;
+        if (t == 0) c = top;
+        else {
+          if (w2 == 0u || (long long)nd >= slots || budget <= 0 || free <= 0) break;
+          c = lshfl(rc, __ffs(w2) - 1);
+        }
+        const int pos = phys(c.k);
+        const int pend = p.w_pend[pos];
+        const int need = blocks(pend);
+        if (need > free) { taken = -1; break; }
+        if (lane == 0) p.l_a[nd] = pos;
+        nd++;
+        free -= need;
+        budget -= min((long long)pend, budget);
+        last = c;
+        have_last = true;
+        taken++;
+      }
+      if (taken < 2) break;  // stopped, or the queue has no third candidate to try yet
+      if (w2 == 0u) break;
     }
     __syncwarp();
     return nd;
@@ -537,26 +807,42 @@ struct Eng {
       V += __popc(m);
     }
     __syncwarp();
-    for (int i = lane; i < V; i += 32) {  // descending key == (-remaining, -dispatch_seq)
-      const unsigned long long k = p.v_key[i];
-      int rank = 0;
-      for (int u = 0; u < V; ++u) rank += p.v_key[u] > k;
-      const int j = (int)(unsigned)k;
-      p.v_idx[rank] = j;
-      p.v_rem[rank] = (int)(k >> 32);
-      p.v_cum[rank] = blocks(p.r_prompt[j] + p.r_gen[j]);
+    // descending key == (-remaining, -dispatch_seq)
+    if (V <= 32) {
+      unsigned long long x[1] = {lane < V ? p.v_key[lane] : 0ULL};
+      warp_sort_desc<1>(x, lane);
+      victims_write(x[0], lane, V);
+    } else if (V <= 256) {
+      sort_keys_desc_256(p.v_key, V);
+      for (int i = lane; i < V; i += 32) victims_write(p.v_key[i], i, V);
+    } else {
+      for (int i = lane; i < V; i += 32) {  // rare (global tables only): rank sort
+        const unsigned long long k = p.v_key[i];
+        int rank = 0;
+#pragma unroll 1
+        for (int u = 0; u < V; ++u) rank += p.v_key[u] > k;
+        victims_write(k, rank, V);
+      }
     }
     __syncwarp();
-    long long carry = 0;
+    int carry = 0;  // prefix block sums (<= pool blocks: fits 32 bits)
     for (int base = 0; base < V; base += 32) {
-      int i = base + lane;
-      long long b = i < V ? p.v_cum[i] : 0;
-      long long incl = warp_incl_scan_ll(b, lane) + carry;
+      const int i = base + lane;
+      const int b = i < V ? (int)p.v_cum[i] : 0;
+      const int incl = warp_incl_scan(b, lane) + carry;
       if (i < V) p.v_cum[i] = incl;
       carry = __shfl_sync(FULL, incl, 31);
     }
     __syncwarp();
     return V;
+  }
+  __device__ __forceinline__ void victims_write(unsigned long long k, int rank, int V) {
+    if (rank < V) {
+      const int j = (int)(unsigned)k;
+      p.v_idx[rank] = j;
+      p.v_rem[rank] = (int)(k >> 32);
+      p.v_cum[rank] = blocks(p.r_prompt[j] + p.r_gen[j]);
+    }
   }
   // Σ allocated blocks over eligible victims: an upper bound of any candidate's gain
   __device__ long long victims_total() const {
@@ -598,20 +884,67 @@ struct Eng {
     int V = -1;
     int vr = 0x7fffffff;  // victims held in registers when V <= 32: lane v has (remaining, cumulative blocks)
     long long vc = 0;
-    int k0 = 0;
-    while (k0 < st.W) {
+    int bi = 0, s0 = 0;  // walk position: list index, first slot of that block not yet passed
+    while (bi < st.nbl) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;
-      const int k = k0 + lane;
-      const bool v = k < st.W;
-      unsigned long long key = 0;
-      int pend = 0, need = 0;
-      if (v) { key = wkey64()[k]; pend = p.w_pend[k]; need = blocks(pend); }
+      {  // skip test for 32 blocks at once (one per lane): min need > free + G(first remaining key)
+        const int j = bi + lane;
+        const bool valid = j < st.nbl;
+        int bmin = 0x7fffffff;
+        unsigned long long first = ~0ULL;
+        if (valid) {
+          const int bj = p.b_list[j];
+          bmin = p.bm_min[bj];
+          first = (lane == 0 && s0 > 0) ? p.bk_key[bj * 32 + s0] : p.bm_first[bj];
+        }
+        bool keep = valid && bmin <= free;
+        if (can_preempt && __any_sync(FULL, valid && !keep)) {
+          if (V < 0) {
+            V = build_victims();
+#ifdef SSB_PHASE_TIMING
+            tc[6] += 1; tc[7] += V;
+#endif
+            vr = lane < V ? p.v_rem[lane] : -1;
+            vc = lane < V ? p.v_cum[lane] : 0;
+          }
+          const int rem0 = (int)(first >> 32);
+          long long g0;
+          if (V <= 32) {
+            int m0 = 0;
+#pragma unroll 1
+            for (int u = 0; u < V; ++u) m0 += __shfl_sync(FULL, vr, u) > rem0;
+            g0 = __shfl_sync(FULL, vc, m0 > 0 ? m0 - 1 : 0);
+            if (m0 == 0) g0 = 0;
+          } else {
+            const int m0 = valid ? victims_above(V, rem0) : 0;
+            g0 = m0 > 0 ? p.v_cum[m0 - 1] : 0;
+          }
+          keep = keep || (valid && (long long)bmin <= (long long)free + g0);
+        }
+        const unsigned mk = __ballot_sync(FULL, keep);
+#ifdef SSB_PHASE_TIMING
+        tm[6] += 1;
+#endif
+        if (mk == 0u) { bi += 32; s0 = 0; continue; }
+        const int first_keep = __ffs(mk) - 1;
+        if (first_keep > 0) { bi += first_keep; s0 = 0; }
+      }
+      const int b = p.b_list[bi];
+      const int cnt = p.bm_cnt[b];
+      unsigned long long key;
+      int rid, pend;
+      blk_load(b, cnt, key, rid, pend);
+#ifdef SSB_PHASE_TIMING
+      tm[7] += 1;
+#endif
+      const bool v = lane >= s0 && lane < cnt;
+      const int need = v ? blocks(pend) : 0;
       const int rem = (int)(key >> 32);
       const bool fit = v && need <= free;
       const unsigned mfit = __ballot_sync(FULL, fit);
       const int ffit = mfit ? __ffs(mfit) - 1 : 32;
       int act = ffit;
-      if (can_preempt && ffit > 0) {
+      if (can_preempt && __any_sync(FULL, v && lane < ffit)) {
         if (V < 0) {
           V = build_victims();
           vr = lane < V ? p.v_rem[lane] : -1;
@@ -619,7 +952,7 @@ struct Eng {
         }
         // G(rem) = blocks of eligible victims with remaining > rem: non-increasing in rem, and the
         // chunk's candidates are in ascending rem, so G(first candidate) bounds the whole chunk
-        const int rem0 = __shfl_sync(FULL, rem, 0);
+        const int rem0 = __shfl_sync(FULL, rem, s0 & 31);
         long long g0;
         if (V <= 32) {
           const int m0 = __popc(__ballot_sync(FULL, vr > rem0));
@@ -633,6 +966,7 @@ struct Eng {
           long long gain;
           if (V <= 32) {
             int m = 0;
+#pragma unroll 1
             for (int u = 0; u < V; ++u) m += __shfl_sync(FULL, vr, u) > rem;
             gain = __shfl_sync(FULL, vc, m > 0 ? m - 1 : 0);
             if (m == 0) gain = 0;
@@ -644,12 +978,11 @@ struct Eng {
           if (mcov) act = __ffs(mcov) - 1;
         }
       }
-      if (act == 32) { k0 += 32; continue; }
-      const int cpos = k0 + act;
+      if (act == 32) { bi += 1; s0 = 0; continue; }
       const int crem = __shfl_sync(FULL, rem, act);
       const int cpend = __shfl_sync(FULL, pend, act);
+      const int rid_flag = __shfl_sync(FULL, rid, act);
       const int cneed = blocks(cpend);
-      const int rid_flag = p.w_rid[cpos];
       if (cneed > free) {
         // take victims (largest remaining first, youngest first on ties) until free+gain >= need
         const int m = victims_above(V, crem);
@@ -673,8 +1006,8 @@ struct Eng {
       nd++;
       free -= cneed;
       __syncwarp();
-      trail_remove(cpos);  // the next candidate moves into slot cpos
-      k0 = cpos;
+      trail_remove_at(bi, act);  // the next candidate moves into this slot
+      s0 = (cnt == 1) ? 0 : act;  // an emptied block left the list: bi is now its successor
     }
     __syncwarp();
     nd_out = nd;
@@ -730,6 +1063,7 @@ struct Eng {
   __device__ void apply_dispatches(int nd, bool prefix_mode) {
     if (nd == 0) return;
     nodisp = false;
+    lc_valid = false;
     if (st.R + nd > cfg.Rc) { st.status = SSB_E_CAPACITY; return; }
     int need_sum = 0;
     long long pend_sum = 0;
@@ -980,6 +1314,7 @@ struct Eng {
       bool in = j < st.R && p.r_plan[j] == 1;
       progress_group<false>(j, in, removed);
     }
+    if (nq) flush_pushes();
     return removed;
   }
 
@@ -1143,6 +1478,7 @@ struct Eng {
     if (!has_work()) { st.status = SSB_E_STALL; return; }
     int nd = 0, np = 0;
     bool prefix = false;
+    SSB_T0(sel)
     if (!nodisp) {
       switch (cfg.policy) {
         case SSB_POLICY_FCFS:
@@ -1157,7 +1493,9 @@ struct Eng {
       // nothing dispatched: stays so until an enqueue / dispatch / finish / preempt
       // (larry's order moves with the clock, so only an empty queue is stable)
       if (nd == 0 && np == 0) nodisp = cfg.policy != SSB_POLICY_LARRY || st.W == 0;
+      SSB_T1(sel, 1)
     }
+    SSB_T0(disp)
     if (np > 0) {  // policy preempts first (engine.py:203-204), in decision order
       drop_regs();
       for (int t = 0; t < np; ++t) {
@@ -1166,6 +1504,7 @@ struct Eng {
             vf = p.r_pfd[j];
         preempt_entry(j, vrid, vpr, vout, vg, vf, vs, SSB_EV_PREEMPT);
       }
+      flush_pushes();
       compact_running();
     }
     if (nd > 0) {
@@ -1173,12 +1512,14 @@ struct Eng {
       apply_dispatches(nd, prefix);  // then dispatches (engine.py:205-206)
       if (st.status) return;
     }
+    if (np > 0 || nd > 0) { SSB_T1(disp, 2) }
+    SSB_T0(bat)
     if (st.R > 0 && st.R <= 64 && st.ndec == st.R && st.R <= cfg.cap && cfg.bs_shift >= 0) {
       if (!regs_ok) load_regs();
-      if (fast_decode()) return;
+      if (fast_decode()) { SSB_T1(bat, 3) return; }
     }
     drop_regs();
-    if (st.R <= 32) { batch_progress_small(); return; }
+    if (st.R <= 32) { batch_progress_small(); SSB_T1(bat, 4) return; }
     int total, nent, npf;
     long long resident;
     form_batch(total, resident, nent, npf);
@@ -1194,6 +1535,7 @@ struct Eng {
     if (removed) compact_running();
     if (total > st.peak) st.peak = total;
     st.iterations += 1;
+    SSB_T1(bat, 5)
   }
 
   // ---- advance: process every boundary with time < t_lim (cluster.py:142-157 / engine.py:256-265) ----
@@ -1203,6 +1545,9 @@ struct Eng {
     return arrival_of(rid);
   }
   __device__ void advance(double t_lim, int n_avail) {
+#ifdef SSB_PHASE_TIMING
+    for (int i = 0; i < 8; ++i) tm[i] = tc[i] = 0;
+#endif
     init_modes();
     double next_t = next_arrival(n_avail);
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -1217,13 +1562,20 @@ struct Eng {
       if (!(nb < t_lim)) break;  // ties: arrivals before boundaries (cluster.py:62)
       st.clock = nb;             // advance_to (engine.py:186-191)
       if (next_t <= st.clock) {
+        SSB_T0(enq)
         enqueue_ready(n_avail);
+        SSB_T1(enq, 0)
         if (st.status) break;
         next_t = next_arrival(n_avail);
       }
       step();
     }
     drop_regs();  // the table in memory is authoritative between calls
+#ifdef SSB_PHASE_TIMING
+    if (lane == 0)
+      printf("PHASES iters %lld | enq %lld/%lld | sel %lld/%lld | disp %lld/%lld | fast %lld/%lld | small %lld/%lld | gen %lld/%lld | walk %lld/%lld | victims %lld/%lld\n",
+             st.iterations, tm[0], tc[0], tm[1], tc[1], tm[2], tc[2], tm[3], tc[3], tm[4], tc[4], tm[5], tc[5], tm[6], tm[7], tc[6], tc[7]);
+#endif
   }
 };
 

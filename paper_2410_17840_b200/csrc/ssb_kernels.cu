@@ -10,6 +10,7 @@
 //               engine state: at poll instants (p2c, sal) and for sal routes
 //               whose argmin depends on beta. See DESIGN.md §cluster.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -26,10 +27,13 @@ __host__ __device__ inline long long align_up(long long x, long long a) { return
 
 struct Layout {
   long long srv, w_enq, w_rid, w_pend, w_key, r_rid, r_prompt, r_out, r_gen, r_pfd, r_st, r_plan, l_a, l_b, v_idx,
-      v_rem, v_cum, v_key, l_c, rl, total;
+      v_rem, v_cum, v_key, l_c, bk_key, bk_rid, bk_pend, bm_cnt, bm_min, bm_first, bm_last, b_list, b_free, rl,
+      total;
 };
 
-__host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers) {
+__host__ __device__ inline long long trail_blocks(long long Wc) { return Wc / 4 + 16; }
+
+__host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers, int policy) {
   Layout L;
   long long o = 0;
   L.srv = o;      o = align_up(o + (long long)sizeof(Srv), 64);
@@ -51,6 +55,16 @@ __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long l
   L.v_cum = o;    o = align_up(o + 8 * Rc, 64);
   L.v_key = o;    o = align_up(o + 8 * Rc, 64);
   L.l_c = o;      o = align_up(o + 4 * Rc, 64);
+  const long long NB = policy == SSB_POLICY_TRAIL_PLUS ? trail_blocks(Wc) : 0;
+  L.bk_key = o;   o = align_up(o + 8 * 32 * NB, 64);
+  L.bk_rid = o;   o = align_up(o + 4 * 32 * NB, 64);
+  L.bk_pend = o;  o = align_up(o + 4 * 32 * NB, 64);
+  L.bm_cnt = o;   o = align_up(o + 4 * NB, 64);
+  L.bm_min = o;   o = align_up(o + 4 * NB, 64);
+  L.bm_first = o; o = align_up(o + 8 * NB, 64);
+  L.bm_last = o;  o = align_up(o + 8 * NB, 64);
+  L.b_list = o;   o = align_up(o + 4 * NB, 64);
+  L.b_free = o;   o = align_up(o + 4 * NB, 64);
   L.rl = o;       o = align_up(o + (n_servers > 1 ? 4 * N : 0), 64);
   L.total = align_up(o, 256);
   return L;
@@ -76,6 +90,15 @@ __device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
   p.v_cum = (long long*)(base + L.v_cum);
   p.v_key = (unsigned long long*)(base + L.v_key);
   p.l_c = (int*)(base + L.l_c);
+  p.bk_key = (unsigned long long*)(base + L.bk_key);
+  p.bk_rid = (int*)(base + L.bk_rid);
+  p.bk_pend = (int*)(base + L.bk_pend);
+  p.bm_cnt = (int*)(base + L.bm_cnt);
+  p.bm_min = (int*)(base + L.bm_min);
+  p.bm_first = (unsigned long long*)(base + L.bm_first);
+  p.bm_last = (unsigned long long*)(base + L.bm_last);
+  p.b_list = (int*)(base + L.b_list);
+  p.b_free = (int*)(base + L.b_free);
   p.rl = (int*)(base + L.rl);
   return p;
 }
@@ -94,6 +117,7 @@ __device__ inline Cfg make_cfg(const ssb_instance& I) {
   c.n_servers = I.n_servers;
   c.Wc = I.wait_cap;
   c.Rc = I.run_cap;
+  c.NB = e.policy == SSB_POLICY_TRAIL_PLUS ? (int)trail_blocks(I.wait_cap) : 0;
   c.alpha = e.alpha;
   c.c = e.c;
   c.mem_base = e.mem_base_s;
@@ -111,6 +135,7 @@ __device__ inline void init_srv(Srv& s, const Cfg& c) {
   s.wpend_sum = s.fin_in = s.fin_out = s.fin_cnt = s.enq_prompt_sum = s.ev_n = s.pf_pend = 0;
   s.free_blocks = c.pool;
   s.R = s.W = s.whead = s.committed = s.next_arr = s.status = s.ndec = 0;
+  s.nbl = s.nfree = s.nalloc = 0;
 }
 
 // shared running table columns: r_rid r_prompt r_out r_gen r_pfd r_st r_plan l_a l_b
@@ -184,50 +209,80 @@ __device__ inline void clear_records(const Eng& E, long long N, int lane_base, i
 // ------------------------------------------------------------------------
 // single-server instances: one warp each, persistent
 // ------------------------------------------------------------------------
-__global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA)
-k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, int n_order,
-          int* __restrict__ queue, ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
-          unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap, int64_t* ev_count) {
-  extern __shared__ int sm_engines[];
+__device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ inst, int idx, ssb_trace tr,
+                                             ssb_records rec, ssb_stats* __restrict__ stats,
+                                             unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
+                                             int64_t* ev_count, int* sm_tab) {
   const int lane = lane_id();
-  int* sm_tab = sm_engines + (threadIdx.x >> 5) * (SM_COLS * RS);
-  while (true) {
+  const long long t0 = clock64();
+  const ssb_instance I = inst[idx];
+  const Cfg cfg = make_cfg(I);
+  const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine.policy);
+  Eng E;
+  bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap, sm_tab);
+  clear_records(E, I.n_requests, lane, 32);
+  fill_events(E, lane, 32);
+  init_srv(E.st, cfg);
+  __syncwarp();
+  E.advance(__longlong_as_double(0x7ff0000000000000LL), (int)I.n_requests);  // t_lim = +inf
+  if (E.st.status == SSB_OK && (E.st.finished != I.n_requests || E.has_work())) E.st.status = SSB_E_INVARIANT;
+  if (lane == 0) {
+    ssb_stats s;
+    s.iterations = E.st.iterations;
+    s.request_steps = E.st.rsteps;
+    s.batch_tokens = E.st.btokens;
+    s.dispatches = E.st.dispatches;
+    s.preempts = E.st.preempts;
+    s.parks = E.st.parks;
+    s.finished = E.st.finished;
+    s.peak_batch_tokens = E.st.peak;
+    unsigned long long h = FNV_OFF;
+    h ^= E.st.digest; h *= FNV_PRIME;
+    s.digest = h;
+    s.status = E.st.status;
+    s._pad = 0;
+    s.device_cycles = clock64() - t0;
+    stats[idx] = s;
+    if (ev_count) ev_count[idx] = E.st.ev_n;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ unsigned sm_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// Persistent single-server kernel. The host assigns each SM a policy (SMs split in
+// proportion to each policy's estimated work); a warp serves the queue of its SM's policy,
+// longest estimated cost first, and steals from the other queues once its own is empty.
+// Keeping one policy per SM keeps the policy-specific code of each SM's warps the same.
+struct EngineQueues {
+  int n[4];      // instances per policy
+  int off[4];    // offset of each policy's order list in order[]
+};
+__global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA, 1)
+k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, EngineQueues qs,
+          int* __restrict__ queue, const unsigned char* __restrict__ sm_policy, int n_sm_policy, ssb_trace tr,
+          ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch, ssb_event* events,
+          long long ev_cap, int64_t* ev_count) {
+  extern __shared__ int sm_engines[];
+  int* sm_tab = sm_engines + (threadIdx.x >> 5) * (SM_COLS * RS);  // this warp's running table
+  const int lane = lane_id();
+  const unsigned smid = sm_id();
+  int pol = smid < (unsigned)n_sm_policy ? sm_policy[smid] : 0;
+  int tried = 0;
+  while (tried < 4) {
     int q = 0;
-    if (lane == 0) q = atomicAdd(queue, 1);
+    if (lane == 0) q = atomicAdd(queue + pol, 1);
     q = __shfl_sync(FULL, q, 0);
-    if (q >= n_order) break;
-    const int idx = order[q];
-    const ssb_instance I = inst[idx];
-    const Cfg cfg = make_cfg(I);
-    const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers);
-    Eng E;
-    bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap,
-                sm_tab);
-    clear_records(E, I.n_requests, lane, 32);
-    fill_events(E, lane, 32);
-    init_srv(E.st, cfg);
-    __syncwarp();
-    E.advance(__longlong_as_double(0x7ff0000000000000LL), (int)I.n_requests);  // t_lim = +inf
-    if (E.st.status == SSB_OK && (E.st.finished != I.n_requests || E.has_work())) E.st.status = SSB_E_INVARIANT;
-    if (lane == 0) {
-      ssb_stats s;
-      s.iterations = E.st.iterations;
-      s.request_steps = E.st.rsteps;
-      s.batch_tokens = E.st.btokens;
-      s.dispatches = E.st.dispatches;
-      s.preempts = E.st.preempts;
-      s.parks = E.st.parks;
-      s.finished = E.st.finished;
-      s.peak_batch_tokens = E.st.peak;
-      unsigned long long h = FNV_OFF;
-      h ^= E.st.digest; h *= FNV_PRIME;
-      s.digest = h;
-      s.status = E.st.status;
-      s._pad = 0;
-      stats[idx] = s;
-      if (ev_count) ev_count[idx] = E.st.ev_n;
+    if (q >= qs.n[pol]) {  // this queue is drained: steal from the next one
+      pol = (pol + 1) & 3;
+      tried += 1;
+      continue;
     }
-    __syncwarp();
+    run_instance(inst, order[qs.off[pol] + q], tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab);
   }
 }
 
@@ -310,7 +365,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   const bool tabs_in_smem = smem_tabs != 0;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
   const Cfg cfg = make_cfg(I);
-  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n);
+  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine.policy);
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
 
   // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
@@ -542,7 +597,7 @@ extern "C" size_t ssb_prepare(ssb_instance* h, int32_t n_inst) {
     I.wait_cap = (int32_t)Wc;
     I.run_cap = (int32_t)Rc;
     I.scratch_offset = off;
-    Layout L = make_layout(Wc, Rc, N, I.n_servers);
+    Layout L = make_layout(Wc, Rc, N, I.n_servers, I.engine.policy);
     off += L.total * (long long)std::max(1, I.n_servers);
   }
   return (size_t)off;
@@ -563,46 +618,83 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const ssb_instance& I = h_inst[i];
     if (I.n_servers < 1 || I.n_requests < 0 || I.n_requests > 0x7fffffffLL || I.wait_cap < 1 || I.run_cap < 1)
       return SSB_E_ARG;
-    Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers);
+    Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine.policy);
     need = std::max(need, I.scratch_offset + L.total * (long long)I.n_servers);
     if (I.n_servers == 1) singles.push_back(i); else { multis.push_back(i); max_servers = std::max(max_servers, I.n_servers); }
   }
   if ((long long)scratch_bytes < need) return SSB_E_ARG;
   if (max_servers > 4096) return SSB_E_ARG;
-  std::stable_sort(singles.begin(), singles.end(),
-                   [&](int a, int b) { return h_inst[a].est_cost > h_inst[b].est_cost; });
-  // header: [queue counter][order: singles..., multis...]
-  std::vector<int> hdr(16 + n_inst, 0);
-  for (size_t i = 0; i < singles.size(); ++i) hdr[16 + i] = singles[i];
-  for (size_t i = 0; i < multis.size(); ++i) hdr[16 + singles.size() + i] = multis[i];
+  // Singles: one persistent kernel, SMs partitioned by policy (see k_engines).
+  // Multis: one CTA per instance.
+  std::vector<int> sg[4];
+  for (int i : singles) sg[h_inst[i].engine.policy & 3].push_back(i);
+  double gwork[4] = {0, 0, 0, 0}, total_work = 0;
+  for (int p = 0; p < 4; ++p) {
+    std::stable_sort(sg[p].begin(), sg[p].end(),
+                     [&](int a, int b) { return h_inst[a].est_cost > h_inst[b].est_cost; });
+    for (int i : sg[p]) gwork[p] += (double)std::max(1, h_inst[i].est_cost);
+    total_work += gwork[p];
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // header (ints): [queue counters x4, pad x12][sm policy table (bytes)][singles by policy][multis]
+  const int smtab_ints = (sms + 3) / 4 + 4;
+  std::vector<int> hdr(16 + smtab_ints + n_inst, 0);
+  unsigned char* smpol = (unsigned char*)(hdr.data() + 16);
+  {  // SMs per policy in proportion to estimated work (largest remainder), >= 1 if it has work
+    int cnt[4] = {0, 0, 0, 0}, given = 0;
+    double rem[4];
+    for (int p = 0; p < 4; ++p) {
+      const double want = total_work > 0 ? sms * gwork[p] / total_work : 0.0;
+      cnt[p] = sg[p].empty() ? 0 : std::max(1, (int)want);
+      rem[p] = want - cnt[p];
+      given += cnt[p];
+    }
+    while (given > sms) {
+      int pm = 0;
+      for (int p = 1; p < 4; ++p) if (cnt[p] > cnt[pm]) pm = p;
+      cnt[pm]--; given--;
+    }
+    while (given < sms) {
+      int pm = -1;
+      for (int p = 0; p < 4; ++p) if (!sg[p].empty() && (pm < 0 || rem[p] > rem[pm])) pm = p;
+      if (pm < 0) break;
+      cnt[pm]++; rem[pm] -= 1.0; given++;
+    }
+    int s0 = 0;
+    for (int p = 0; p < 4; ++p) for (int k = 0; k < cnt[p] && s0 < sms; ++k) smpol[s0++] = (unsigned char)p;
+    for (; s0 < sms; ++s0) smpol[s0] = 0;
+  }
+  EngineQueues qs;
+  int o = 16 + smtab_ints;
+  for (int p = 0; p < 4; ++p) { qs.off[p] = o - (16 + smtab_ints); qs.n[p] = (int)sg[p].size(); for (int i : sg[p]) hdr[o++] = i; }
+  const int off_multi = o;
+  for (int i : multis) hdr[o++] = i;
   unsigned char* scratch = (unsigned char*)d_scratch;
   if (cudaMemcpyAsync(scratch, hdr.data(), sizeof(int) * hdr.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess)
     return SSB_E_CUDA;
-  const int* d_order = (const int*)(scratch) + 16;
-  int* d_queue = (int*)scratch;
+  const int* d_hdr = (const int*)scratch;
   if (!multis.empty()) {
-    int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
-    size_t sm = sizeof(long long) * 5 * ((max_servers + 1) & ~1);
-    if (max_servers <= CLUSTER_SMEM_SERVERS) sm += sizeof(int) * SM_COLS * RS * max_servers;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_cluster<<<(unsigned)multis.size(), 32 * nw, sm, stream>>>(d_inst, d_order + singles.size(), trace, records,
-                                                                d_stats, scratch, d_events, event_cap, d_event_count,
-                                                                max_servers <= CLUSTER_SMEM_SERVERS ? 1 : 0);
+    const int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
+    size_t smc = sizeof(long long) * 5 * ((max_servers + 1) & ~1);
+    if (max_servers <= CLUSTER_SMEM_SERVERS) smc += sizeof(int) * SM_COLS * RS * max_servers;
+    if (smc > 48 * 1024) cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+    k_cluster<<<(unsigned)multis.size(), 32 * nw, smc, stream>>>(d_inst, d_hdr + off_multi, trace, records, d_stats,
+                                                               scratch, d_events, event_cap, d_event_count,
+                                                               max_servers <= CLUSTER_SMEM_SERVERS ? 1 : 0);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   if (!singles.empty()) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int occ = 1;
     const size_t sm = sizeof(int) * SM_COLS * RS * ENGINE_WARPS_PER_CTA;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k_engines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engines, 32 * ENGINE_WARPS_PER_CTA, sm);
-    long long want = ((long long)singles.size() + ENGINE_WARPS_PER_CTA - 1) / ENGINE_WARPS_PER_CTA;
-    int grid = (int)std::min<long long>(want, (long long)sms * std::max(1, occ));
-    k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(d_inst, d_order, (int)singles.size(), d_queue, trace,
-                                                              records, d_stats, scratch, d_events, event_cap,
-                                                              d_event_count);
+    if (const char* cap = getenv("SSB_CTAS_PER_SM")) occ = std::min(occ, std::max(1, atoi(cap)));  // experiments
+    const int grid = sms * std::max(1, occ);
+    k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(
+        d_inst, d_hdr + 16 + smtab_ints, qs, (int*)scratch, (const unsigned char*)(d_hdr + 16), sms, trace, records,
+        d_stats, scratch, d_events, event_cap, d_event_count);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   return SSB_OK;

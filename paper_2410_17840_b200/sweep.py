@@ -120,6 +120,14 @@ class SweepRunner:
         self.torch.cuda.synchronize()
         return (self.p_stats.numpy().view(_abi.STATS).copy(), self.p_summary.numpy().view(_abi.SUMMARY).copy())
 
+    def adopt_measured_schedule(self, stats) -> None:
+        """Use each instance's measured device cycles (ssb_stats.device_cycles) as its
+        scheduling hint for later runs of this sweep: per-policy kernel shares of the GPU
+        and longest-first queue order. Work is unchanged; only the placement adapts."""
+        cyc = np.asarray(stats["device_cycles"], dtype=np.int64)
+        if (cyc > 0).all():
+            self.h_inst["est_cost"] = np.clip(cyc // 1024, 1, 2**31 - 1)
+
     def fix_overflows(self) -> int:
         """Re-run instances whose shared running table overflowed (then re-summarize)."""
         n = retry_overflows(self.db)

@@ -2,6 +2,7 @@
 import collections, os, re, subprocess, sys, tempfile
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2410_17840_b200/libssb.so"
 kname = sys.argv[2] if len(sys.argv) > 2 else "k_engines"
+import fnmatch
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
 cub = [f for f in os.listdir(d) if f.endswith(".cubin") and "summary" not in f][0]
