@@ -40,7 +40,7 @@ constexpr unsigned long long FNV_PRIME = 0x100000001b3ULL;
 
 struct Cfg {
   int policy, max_output, bs, bs_shift, pool, cap, max_running, max_ctx;
-  int n_servers, Wc, Rc, NB;
+  int n_servers, Wc, Rc;
   double alpha, c, mem_base, mem_kv, compute, overhead, qps;
 };
 
@@ -55,7 +55,6 @@ struct Srv {
   long long ev_n;
   long long pf_pend;         // Σ pending over PREFILLING entries
   int free_blocks, R, W, whead, committed, next_arr, status, ndec;
-  int nbl, nfree, nalloc;    // trail_plus blocked waiting list: blocks in list / free stack / bump
 };
 
 struct SrvPtr {
@@ -73,16 +72,6 @@ struct SrvPtr {
   int* l_a;   // dispatch list (physical ring slots) / scratch list
   int* l_b;   // preempt list (table indices) / scratch list
   int* l_c;   // trail_plus dispatch list: pending prefill
-  // trail_plus waiting set: ordered list of 32-slot blocks, each sorted by key
-  unsigned long long* bk_key;  // [NB*32] remaining<<32 | id
-  int* bk_rid;                 // [NB*32] id | FLAG_SEEN
-  int* bk_pend;                // [NB*32] pending prefill
-  int* bm_cnt;                 // [NB] entries in the block
-  int* bm_min;                 // [NB] min block need in the block
-  unsigned long long* bm_first;  // [NB] first / last key
-  unsigned long long* bm_last;
-  int* b_list;                 // [NB] block ids in key order
-  int* b_free;                 // [NB] free-block stack
   int* v_idx; // trail_plus victims sorted by (-remaining, -dispatch_seq)
   int* v_rem;
   long long* v_cum;
@@ -149,7 +138,7 @@ __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool
 __device__ __noinline__ int div_up_slow(int t, int bs) { return (t + bs - 1) / bs; }
 
 // FNV-1a over the 64-bit words (code, request id, time bits) of one event
-__device__ __noinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
+__device__ __forceinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
   h ^= (unsigned long long)code; h *= FNV_PRIME;
   h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
   h ^= (unsigned long long)__double_as_longlong(t); h *= FNV_PRIME;
@@ -198,6 +187,7 @@ __device__ __forceinline__ void warp_sort_desc(unsigned long long (&x)[K], int l
   }
 }
 
+#ifdef SSB_SORT256
 // Sort keys[0..n) (n <= 256) descending in place: 8 registers per lane, one bitonic network.
 // Out of line: one copy of the network in the image, register-only interface.
 __device__ __noinline__ void sort_keys_desc_256(unsigned long long* keys, int n) {
@@ -212,6 +202,7 @@ __device__ __noinline__ void sort_keys_desc_256(unsigned long long* keys, int n)
     if (k * 32 + lane < n) keys[k * 32 + lane] = x[k];
   __syncwarp();
 }
+#endif
 
 // stable compaction of a running table (drops ST_GONE entries); returns the new size.
 // Out of line with pointer/int arguments only, so callers keep their state in registers.
@@ -376,145 +367,56 @@ struct Eng {
     st.ev_n += 1;
   }
 
-  // ---- trail_plus waiting set: an ordered list of 32-slot blocks, sorted by key =
-  // (remaining << 32 | id). Insert / remove touch one block (one warp chunk: shuffles);
-  // a full block splits in two, a block under 8 entries merges with its successor when
-  // they fit; per-block (count, min need, first, last key) let the walk skip blocks. ----
-  __device__ __forceinline__ int blk_alloc() {
-    if (st.nfree > 0) return p.b_free[--st.nfree];
-    if (st.nalloc < cfg.NB) return st.nalloc++;
-    st.status = SSB_E_CAPACITY;
-    return 0;
-  }
-  __device__ __forceinline__ void blk_meta(int b, int cnt, unsigned long long key, int pend) {
-    const unsigned mn = __reduce_min_sync(FULL, lane < cnt ? (unsigned)blocks(pend) : 0x7fffffffu);
-    const unsigned long long first = __shfl_sync(FULL, key, 0), last = __shfl_sync(FULL, key, (cnt - 1) & 31);
-    if (lane == 0) { p.bm_cnt[b] = cnt; p.bm_min[b] = (int)mn; p.bm_first[b] = first; p.bm_last[b] = last; }
-  }
-  __device__ __forceinline__ void blk_load(int b, int cnt, unsigned long long& key, int& rid, int& pend) const {
-    key = ~0ULL; rid = 0; pend = 0;
-    if (lane < cnt) { const int s = b * 32 + lane; key = p.bk_key[s]; rid = p.bk_rid[s]; pend = p.bk_pend[s]; }
-  }
-  __device__ __forceinline__ void blk_store(int b, int lo, int hi, unsigned long long key, int rid, int pend) {
-    if (lane >= lo && lane < hi) { const int s = b * 32 + lane; p.bk_key[s] = key; p.bk_rid[s] = rid; p.bk_pend[s] = pend; }
-  }
-  __device__ int blk_find(unsigned long long k) const {  // first block whose last key >= k, else the last
-    for (int base = 0; base < st.nbl; base += 32) {
-      const int i = base + lane;
-      const unsigned m = __ballot_sync(FULL, i < st.nbl && p.bm_last[p.b_list[i]] >= k);
-      if (m) return base + __ffs(m) - 1;
+  // ---- trail_plus waiting set: slots [0, W) sorted by key = (remaining << 32 | id) ----
+  // (whead stays 0; the 64-bit key lives in the w_enq column, rid|flag in w_rid, pending in w_pend)
+  __device__ __forceinline__ unsigned long long* wkey64() const { return reinterpret_cast<unsigned long long*>(p.w_enq); }
+  __device__ int trail_lower_bound(unsigned long long k, int n) const {  // first slot with key >= k
+    int lo = 0, hi = n;
+    while (hi - lo > 32) {  // 32-ary search: one ballot per level
+      const int step = (hi - lo + 31) >> 5;
+      const int pos = lo + lane * step;
+      const unsigned m = __ballot_sync(FULL, pos < hi && wkey64()[pos] < k);
+      const int c = __popc(m);
+      const int nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
+      const int nhi = min(hi, lo + c * step);
+      lo = nlo;
+      hi = nhi;
     }
-    return st.nbl - 1;
-  }
-  __device__ void list_insert(int at, int nb) {
-    for (int hi = st.nbl; hi > at; hi -= 32) {
-      const int i = max(at, hi - 32) + lane;
-      const int x = i < hi ? p.b_list[i] : 0;
-      __syncwarp();
-      if (i < hi) p.b_list[i + 1] = x;
-      __syncwarp();
-    }
-    if (lane == 0) p.b_list[at] = nb;
-    __syncwarp();
-    st.nbl += 1;
-  }
-  __device__ void list_remove(int at) {
-    for (int lo = at + 1; lo < st.nbl; lo += 32) {
-      const int i = lo + lane;
-      const int x = i < st.nbl ? p.b_list[i] : 0;
-      __syncwarp();
-      if (i < st.nbl) p.b_list[i - 1] = x;
-      __syncwarp();
-    }
-    st.nbl -= 1;
-  }
-  __device__ __forceinline__ void blk_release(int b) {
-    if (lane == 0) p.b_free[st.nfree] = b;
-    __syncwarp();
-    st.nfree += 1;
+    const int pos = lo + lane;
+    return lo + __popc(__ballot_sync(FULL, pos < hi && wkey64()[pos] < k));
   }
   __device__ void trail_insert(int rid_flag, int pend, int rem) {
     const unsigned long long k = ((unsigned long long)(unsigned)rem << 32) | (unsigned)(rid_flag & 0x7fffffff);
-    if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
-    if (st.nbl == 0) {
-      const int b = blk_alloc();
-      if (st.status) return;
-      if (lane == 0) p.bm_cnt[b] = 0;
+    const int n = st.W;
+    if (n + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
+    const int pos = trail_lower_bound(k, n);
+    for (int hi = n; hi > pos; hi -= 32) {  // shift [pos, n) up one slot, top chunk first
+      const int lo = max(pos, hi - 32);
+      const int i = lo + lane;
+      const bool v = i < hi;
+      unsigned long long kk = 0;
+      int r = 0, pd = 0;
+      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
       __syncwarp();
-      list_insert(0, b);
-    }
-    int bi = blk_find(k);
-    int b = p.b_list[bi];
-    int cnt = p.bm_cnt[b];
-    unsigned long long key;
-    int rid, pd;
-    blk_load(b, cnt, key, rid, pd);
-    if (cnt == 32) {  // split: the upper half moves to a new block after b
-      const int nb = blk_alloc();
-      if (st.status) return;
-      const unsigned long long ukey = __shfl_down_sync(FULL, key, 16);
-      const int urid = __shfl_down_sync(FULL, rid, 16), upd = __shfl_down_sync(FULL, pd, 16);
-      blk_store(nb, 0, 16, ukey, urid, upd);
-      blk_meta(nb, 16, ukey, upd);
-      blk_meta(b, 16, key, pd);
+      if (v) { wkey64()[i + 1] = kk; p.w_rid[i + 1] = r; p.w_pend[i + 1] = pd; }
       __syncwarp();
-      list_insert(bi + 1, nb);
-      const unsigned long long last_lo = __shfl_sync(FULL, key, 15);
-      cnt = 16;
-      if (k > last_lo) { bi += 1; b = nb; key = ukey; rid = urid; pd = upd; }
-      if (lane >= 16) { key = ~0ULL; rid = 0; pd = 0; }
     }
-    const int pos = __popc(__ballot_sync(FULL, lane < cnt && key < k));
-    const unsigned long long nk = __shfl_up_sync(FULL, key, 1);
-    const int nr = __shfl_up_sync(FULL, rid, 1), np = __shfl_up_sync(FULL, pd, 1);
-    if (lane > pos) { key = nk; rid = nr; pd = np; }
-    if (lane == pos) { key = k; rid = rid_flag; pd = pend; }
-    cnt += 1;
-    blk_store(b, pos, cnt, key, rid, pd);
-    blk_meta(b, cnt, key, pd);
+    if (lane == 0) { wkey64()[pos] = k; p.w_rid[pos] = rid_flag; p.w_pend[pos] = pend; }
     __syncwarp();
-    st.W += 1;
+    st.W = n + 1;
   }
-  // remove slot `pos` of the block at list index bi
-  __device__ void trail_remove_at(int bi, int pos) {
-    const int b = p.b_list[bi];
-    int cnt = p.bm_cnt[b];
-    unsigned long long key;
-    int rid, pd;
-    blk_load(b, cnt, key, rid, pd);
-    const unsigned long long nk = __shfl_down_sync(FULL, key, 1);
-    const int nr = __shfl_down_sync(FULL, rid, 1), np = __shfl_down_sync(FULL, pd, 1);
-    if (lane >= pos) { key = nk; rid = nr; pd = np; }
-    cnt -= 1;
+  __device__ void trail_remove(int pos) {  // shift (pos, W) down one slot
+    for (int lo = pos + 1; lo < st.W; lo += 32) {
+      const int i = lo + lane;
+      const bool v = i < st.W;
+      unsigned long long kk = 0;
+      int r = 0, pd = 0;
+      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
+      __syncwarp();
+      if (v) { wkey64()[i - 1] = kk; p.w_rid[i - 1] = r; p.w_pend[i - 1] = pd; }
+      __syncwarp();
+    }
     st.W -= 1;
-    if (cnt == 0) {
-      list_remove(bi);
-      blk_release(b);
-      return;
-    }
-    if (lane >= cnt) { key = ~0ULL; rid = 0; pd = 0; }
-    blk_store(b, pos, cnt, key, rid, pd);
-    if (cnt < 8 && bi + 1 < st.nbl) {  // merge the successor in when both fit
-      const int nb = p.b_list[bi + 1];
-      const int ncnt = p.bm_cnt[nb];
-      if (cnt + ncnt <= 32) {
-        unsigned long long k2;
-        int r2, p2;
-        blk_load(nb, ncnt, k2, r2, p2);
-        const unsigned long long mk = __shfl_up_sync(FULL, k2, cnt);
-        const int mr = __shfl_up_sync(FULL, r2, cnt), mp = __shfl_up_sync(FULL, p2, cnt);
-        if (lane >= cnt && lane < cnt + ncnt) { key = mk; rid = mr; pd = mp; }
-        blk_store(b, cnt, cnt + ncnt, key, rid, pd);
-        cnt += ncnt;
-        blk_meta(b, cnt, key, pd);
-        __syncwarp();
-        list_remove(bi + 1);
-        blk_release(nb);
-        return;
-      }
-    }
-    blk_meta(b, cnt, key, pd);
-    __syncwarp();
   }
 
   // ---- Engine.enqueue for every routed arrival with arrival <= clock (engine.py:175-184, 261-262) ----
@@ -808,15 +710,19 @@ struct Eng {
     }
     __syncwarp();
     // descending key == (-remaining, -dispatch_seq)
-    if (V <= 32) {
-      unsigned long long x[1] = {lane < V ? p.v_key[lane] : 0ULL};
-      warp_sort_desc<1>(x, lane);
-      victims_write(x[0], lane, V);
+    if (V <= 32) {  // rank sort in registers: V shuffle steps (V is usually a handful)
+      const unsigned long long k = lane < V ? p.v_key[lane] : 0ULL;
+      int rank = 0;
+#pragma unroll 1
+      for (int u = 0; u < V; ++u) rank += __shfl_sync(FULL, k, u) > k;
+      if (lane < V) victims_write(k, rank, V);
+#ifdef SSB_SORT256
     } else if (V <= 256) {
       sort_keys_desc_256(p.v_key, V);
       for (int i = lane; i < V; i += 32) victims_write(p.v_key[i], i, V);
+#endif
     } else {
-      for (int i = lane; i < V; i += 32) {  // rare (global tables only): rank sort
+      for (int i = lane; i < V; i += 32) {  // larger victim sets: rank sort in shared memory
         const unsigned long long k = p.v_key[i];
         int rank = 0;
 #pragma unroll 1
@@ -884,67 +790,20 @@ struct Eng {
     int V = -1;
     int vr = 0x7fffffff;  // victims held in registers when V <= 32: lane v has (remaining, cumulative blocks)
     long long vc = 0;
-    int bi = 0, s0 = 0;  // walk position: list index, first slot of that block not yet passed
-    while (bi < st.nbl) {
+    int k0 = 0;
+    while (k0 < st.W) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;
-      {  // skip test for 32 blocks at once (one per lane): min need > free + G(first remaining key)
-        const int j = bi + lane;
-        const bool valid = j < st.nbl;
-        int bmin = 0x7fffffff;
-        unsigned long long first = ~0ULL;
-        if (valid) {
-          const int bj = p.b_list[j];
-          bmin = p.bm_min[bj];
-          first = (lane == 0 && s0 > 0) ? p.bk_key[bj * 32 + s0] : p.bm_first[bj];
-        }
-        bool keep = valid && bmin <= free;
-        if (can_preempt && __any_sync(FULL, valid && !keep)) {
-          if (V < 0) {
-            V = build_victims();
-#ifdef SSB_PHASE_TIMING
-            tc[6] += 1; tc[7] += V;
-#endif
-            vr = lane < V ? p.v_rem[lane] : -1;
-            vc = lane < V ? p.v_cum[lane] : 0;
-          }
-          const int rem0 = (int)(first >> 32);
-          long long g0;
-          if (V <= 32) {
-            int m0 = 0;
-#pragma unroll 1
-            for (int u = 0; u < V; ++u) m0 += __shfl_sync(FULL, vr, u) > rem0;
-            g0 = __shfl_sync(FULL, vc, m0 > 0 ? m0 - 1 : 0);
-            if (m0 == 0) g0 = 0;
-          } else {
-            const int m0 = valid ? victims_above(V, rem0) : 0;
-            g0 = m0 > 0 ? p.v_cum[m0 - 1] : 0;
-          }
-          keep = keep || (valid && (long long)bmin <= (long long)free + g0);
-        }
-        const unsigned mk = __ballot_sync(FULL, keep);
-#ifdef SSB_PHASE_TIMING
-        tm[6] += 1;
-#endif
-        if (mk == 0u) { bi += 32; s0 = 0; continue; }
-        const int first_keep = __ffs(mk) - 1;
-        if (first_keep > 0) { bi += first_keep; s0 = 0; }
-      }
-      const int b = p.b_list[bi];
-      const int cnt = p.bm_cnt[b];
-      unsigned long long key;
-      int rid, pend;
-      blk_load(b, cnt, key, rid, pend);
-#ifdef SSB_PHASE_TIMING
-      tm[7] += 1;
-#endif
-      const bool v = lane >= s0 && lane < cnt;
-      const int need = v ? blocks(pend) : 0;
+      const int k = k0 + lane;
+      const bool v = k < st.W;
+      unsigned long long key = 0;
+      int pend = 0, need = 0;
+      if (v) { key = wkey64()[k]; pend = p.w_pend[k]; need = blocks(pend); }
       const int rem = (int)(key >> 32);
       const bool fit = v && need <= free;
       const unsigned mfit = __ballot_sync(FULL, fit);
       const int ffit = mfit ? __ffs(mfit) - 1 : 32;
       int act = ffit;
-      if (can_preempt && __any_sync(FULL, v && lane < ffit)) {
+      if (can_preempt && ffit > 0) {
         if (V < 0) {
           V = build_victims();
           vr = lane < V ? p.v_rem[lane] : -1;
@@ -952,7 +811,7 @@ struct Eng {
         }
         // G(rem) = blocks of eligible victims with remaining > rem: non-increasing in rem, and the
         // chunk's candidates are in ascending rem, so G(first candidate) bounds the whole chunk
-        const int rem0 = __shfl_sync(FULL, rem, s0 & 31);
+        const int rem0 = __shfl_sync(FULL, rem, 0);
         long long g0;
         if (V <= 32) {
           const int m0 = __popc(__ballot_sync(FULL, vr > rem0));
@@ -978,11 +837,12 @@ struct Eng {
           if (mcov) act = __ffs(mcov) - 1;
         }
       }
-      if (act == 32) { bi += 1; s0 = 0; continue; }
+      if (act == 32) { k0 += 32; continue; }
+      const int cpos = k0 + act;
       const int crem = __shfl_sync(FULL, rem, act);
       const int cpend = __shfl_sync(FULL, pend, act);
-      const int rid_flag = __shfl_sync(FULL, rid, act);
       const int cneed = blocks(cpend);
+      const int rid_flag = p.w_rid[cpos];
       if (cneed > free) {
         // take victims (largest remaining first, youngest first on ties) until free+gain >= need
         const int m = victims_above(V, crem);
@@ -1006,8 +866,8 @@ struct Eng {
       nd++;
       free -= cneed;
       __syncwarp();
-      trail_remove_at(bi, act);  // the next candidate moves into this slot
-      s0 = (cnt == 1) ? 0 : act;  // an emptied block left the list: bi is now its successor
+      trail_remove(cpos);  // the next candidate moves into slot cpos
+      k0 = cpos;
     }
     __syncwarp();
     nd_out = nd;

@@ -27,11 +27,8 @@ __host__ __device__ inline long long align_up(long long x, long long a) { return
 
 struct Layout {
   long long srv, w_enq, w_rid, w_pend, w_key, r_rid, r_prompt, r_out, r_gen, r_pfd, r_st, r_plan, l_a, l_b, v_idx,
-      v_rem, v_cum, v_key, l_c, bk_key, bk_rid, bk_pend, bm_cnt, bm_min, bm_first, bm_last, b_list, b_free, rl,
-      total;
+      v_rem, v_cum, v_key, l_c, rl, total;
 };
-
-__host__ __device__ inline long long trail_blocks(long long Wc) { return Wc / 4 + 16; }
 
 __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers, int policy) {
   Layout L;
@@ -55,16 +52,7 @@ __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long l
   L.v_cum = o;    o = align_up(o + 8 * Rc, 64);
   L.v_key = o;    o = align_up(o + 8 * Rc, 64);
   L.l_c = o;      o = align_up(o + 4 * Rc, 64);
-  const long long NB = policy == SSB_POLICY_TRAIL_PLUS ? trail_blocks(Wc) : 0;
-  L.bk_key = o;   o = align_up(o + 8 * 32 * NB, 64);
-  L.bk_rid = o;   o = align_up(o + 4 * 32 * NB, 64);
-  L.bk_pend = o;  o = align_up(o + 4 * 32 * NB, 64);
-  L.bm_cnt = o;   o = align_up(o + 4 * NB, 64);
-  L.bm_min = o;   o = align_up(o + 4 * NB, 64);
-  L.bm_first = o; o = align_up(o + 8 * NB, 64);
-  L.bm_last = o;  o = align_up(o + 8 * NB, 64);
-  L.b_list = o;   o = align_up(o + 4 * NB, 64);
-  L.b_free = o;   o = align_up(o + 4 * NB, 64);
+  (void)policy;
   L.rl = o;       o = align_up(o + (n_servers > 1 ? 4 * N : 0), 64);
   L.total = align_up(o, 256);
   return L;
@@ -90,15 +78,6 @@ __device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
   p.v_cum = (long long*)(base + L.v_cum);
   p.v_key = (unsigned long long*)(base + L.v_key);
   p.l_c = (int*)(base + L.l_c);
-  p.bk_key = (unsigned long long*)(base + L.bk_key);
-  p.bk_rid = (int*)(base + L.bk_rid);
-  p.bk_pend = (int*)(base + L.bk_pend);
-  p.bm_cnt = (int*)(base + L.bm_cnt);
-  p.bm_min = (int*)(base + L.bm_min);
-  p.bm_first = (unsigned long long*)(base + L.bm_first);
-  p.bm_last = (unsigned long long*)(base + L.bm_last);
-  p.b_list = (int*)(base + L.b_list);
-  p.b_free = (int*)(base + L.b_free);
   p.rl = (int*)(base + L.rl);
   return p;
 }
@@ -117,7 +96,6 @@ __device__ inline Cfg make_cfg(const ssb_instance& I) {
   c.n_servers = I.n_servers;
   c.Wc = I.wait_cap;
   c.Rc = I.run_cap;
-  c.NB = e.policy == SSB_POLICY_TRAIL_PLUS ? (int)trail_blocks(I.wait_cap) : 0;
   c.alpha = e.alpha;
   c.c = e.c;
   c.mem_base = e.mem_base_s;
@@ -135,7 +113,6 @@ __device__ inline void init_srv(Srv& s, const Cfg& c) {
   s.wpend_sum = s.fin_in = s.fin_out = s.fin_cnt = s.enq_prompt_sum = s.ev_n = s.pf_pend = 0;
   s.free_blocks = c.pool;
   s.R = s.W = s.whead = s.committed = s.next_arr = s.status = s.ndec = 0;
-  s.nbl = s.nfree = s.nalloc = 0;
 }
 
 // shared running table columns: r_rid r_prompt r_out r_gen r_pfd r_st r_plan l_a l_b
