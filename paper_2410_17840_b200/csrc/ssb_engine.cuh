@@ -138,7 +138,7 @@ __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool
 __device__ __noinline__ int div_up_slow(int t, int bs) { return (t + bs - 1) / bs; }
 
 // FNV-1a over the 64-bit words (code, request id, time bits) of one event
-__device__ __forceinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
+__device__ __noinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
   h ^= (unsigned long long)code; h *= FNV_PRIME;
   h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
   h ^= (unsigned long long)__double_as_longlong(t); h *= FNV_PRIME;
@@ -1020,8 +1020,13 @@ struct Eng {
   // (exclusive scan of released-minus-grown blocks); every lane before the first
   // failing grow commits in parallel; the failing one runs the serial eviction
   // cascade (_grow_or_evict / _evict_for_blocks) and the chunk restarts after it.
+#ifdef SSB_PROGRESS_TEMPLATE
   template <bool PREFILL>
   __device__ void progress_group(int j_lane, bool in_group, bool& removed_any) {
+#else
+  // one body for both sections (runtime flag): halves this cold path's instruction footprint
+  __device__ void progress_group(const bool PREFILL, int j_lane, bool in_group, bool& removed_any) {
+#endif
     int start = 0;
     while (true) {
       int rid = 0, pr = 0, out = 0, g = 0, f = 0, s = ST_GONE, plan = 0;
@@ -1166,13 +1171,21 @@ struct Eng {
     for (int base = 0; base < npf; base += 32) {
       int i = base + lane;
       int j = i < npf ? p.l_b[i] : 0;
+#ifdef SSB_PROGRESS_TEMPLATE
       progress_group<true>(j, i < npf, removed);
+#else
+      progress_group(true, j, i < npf, removed);
+#endif
     }
     // then decode tokens in plan order
     for (int base = 0; base < st.R; base += 32) {
       int j = base + lane;
       bool in = j < st.R && p.r_plan[j] == 1;
+#ifdef SSB_PROGRESS_TEMPLATE
       progress_group<false>(j, in, removed);
+#else
+      progress_group(false, j, in, removed);
+#endif
     }
     if (nq) flush_pushes();
     return removed;
