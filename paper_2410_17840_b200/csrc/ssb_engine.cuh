@@ -38,10 +38,45 @@ constexpr int FLAG_SEEN = (int)0x80000000;  // waiting entry was dispatched befo
 constexpr unsigned long long FNV_OFF = 0xcbf29ce484222325ULL;
 constexpr unsigned long long FNV_PRIME = 0x100000001b3ULL;
 
+// trail_plus waiting set geometry: one bucket per remaining-output value
+// (remaining <= output_len < min(max_context, pool tokens), policies.py:56-68 feasibility),
+// a min-need tree over the buckets with fan-out 32 (one warp ballot per level).
+// Level l holds n_l = ceil(n_{l-1}/32) nodes, padded to a multiple of 32; the top level
+// fits one warp (<= 32 nodes).
+struct TrailGeom {
+  int nb;      // buckets (multiple of 32)
+  int top;     // index of the top level (0..3)
+  int off[4];  // level offsets (ints) into the level array
+  int total;   // ints in the level array
+};
+__host__ __device__ inline TrailGeom trail_geom(int max_ctx, int pool, int bs) {
+  long long maxrem = (long long)pool * bs;
+  if ((long long)max_ctx < maxrem) maxrem = max_ctx;
+  if (maxrem < 1) maxrem = 1;
+  TrailGeom g;
+  long long n = (maxrem + 32) / 32 * 32;  // buckets 0..maxrem
+  if (n > (1LL << 20)) n = 1LL << 20;     // 4 levels at most (ssb_simulate rejects larger)
+  g.nb = (int)n;
+  g.top = 0;
+  g.off[0] = 0;
+  g.off[1] = g.off[2] = g.off[3] = 0;
+  long long o = n;
+  while (n > 32 && g.top < 3) {
+    n = (n + 31) / 32;
+    n = (n + 31) / 32 * 32;
+    g.top += 1;
+    g.off[g.top] = (int)o;
+    o += n;
+  }
+  g.total = (int)o;
+  return g;
+}
+
 struct Cfg {
   int policy, max_output, bs, bs_shift, pool, cap, max_running, max_ctx;
   int n_servers, Wc, Rc;
   double alpha, c, mem_base, mem_kv, compute, overhead, qps;
+  TrailGeom tg;
 };
 
 // Persisted per-engine state (global scratch; registers while a warp runs it).
@@ -72,11 +107,13 @@ struct SrvPtr {
   int* l_a;   // dispatch list (physical ring slots) / scratch list
   int* l_b;   // preempt list (table indices) / scratch list
   int* l_c;   // trail_plus dispatch list: pending prefill
-  int* v_idx; // trail_plus victims sorted by (-remaining, -dispatch_seq)
-  int* v_rem;
-  long long* v_cum;
-  unsigned long long* v_key;  // unsorted compact victim keys (scratch)
+  int* v_idx; // queued waiting pushes (preempt_entry / flush_pushes): rid | flag
+  int* v_rem; //   ... pending prefill
+  long long* v_cum;           //   ... policy key; trail_plus victims: allocated blocks
+  unsigned long long* v_key;  // trail_plus victims: (remaining << 32 | table index), 0 = taken
   int* rl;    // route list (arrival ids routed to this engine), n_servers > 1
+  int* t_head;  // trail_plus: first request id of each remaining-output bucket (-1 = empty)
+  int* t_lv;    // trail_plus: min-need tree over the buckets (level 0 = per-bucket minimum)
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -155,54 +192,6 @@ __device__ __noinline__ void write_event(ssb_event* ev, long long pos, long long
     ev[pos] = e;
   }
 }
-
-// Warp bitonic sort, descending, of 32*K 64-bit keys held in registers: element i = k*32 + lane.
-// Pad unused elements with 0 (they sort last).
-template <int K>
-__device__ __forceinline__ void warp_sort_desc(unsigned long long (&x)[K], int lane) {
-#pragma unroll
-  for (int size = 2; size <= 32 * K; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int i = k * 32 + lane;
-        const bool desc = (i & size) == 0;  // this size-block is sorted descending
-        if (stride >= 32) {
-          const int kj = k ^ (stride >> 5);
-          if (kj > k) {
-            const unsigned long long a = x[k], b = x[kj];
-            const bool sw = desc ? (a < b) : (a > b);
-            x[k] = sw ? b : a;
-            x[kj] = sw ? a : b;
-          }
-        } else {
-          const unsigned long long o = __shfl_xor_sync(FULL, x[k], stride);
-          const bool lower = (i & stride) == 0;
-          const bool keep_max = lower == desc;
-          x[k] = keep_max ? (x[k] > o ? x[k] : o) : (x[k] < o ? x[k] : o);
-        }
-      }
-    }
-  }
-}
-
-#ifdef SSB_SORT256
-// Sort keys[0..n) (n <= 256) descending in place: 8 registers per lane, one bitonic network.
-// Out of line: one copy of the network in the image, register-only interface.
-__device__ __noinline__ void sort_keys_desc_256(unsigned long long* keys, int n) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long x[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) x[k] = (k * 32 + lane < n) ? keys[k * 32 + lane] : 0ULL;
-  warp_sort_desc<8>(x, lane);
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (k * 32 + lane < n) keys[k * 32 + lane] = x[k];
-  __syncwarp();
-}
-#endif
 
 // stable compaction of a running table (drops ST_GONE entries); returns the new size.
 // Out of line with pointer/int arguments only, so callers keep their state in registers.
@@ -367,54 +356,89 @@ struct Eng {
     st.ev_n += 1;
   }
 
-  // ---- trail_plus waiting set: slots [0, W) sorted by key = (remaining << 32 | id) ----
-  // (whead stays 0; the 64-bit key lives in the w_enq column, rid|flag in w_rid, pending in w_pend)
-  __device__ __forceinline__ unsigned long long* wkey64() const { return reinterpret_cast<unsigned long long*>(p.w_enq); }
-  __device__ int trail_lower_bound(unsigned long long k, int n) const {  // first slot with key >= k
-    int lo = 0, hi = n;
-    while (hi - lo > 32) {  // 32-ary search: one ballot per level
-      const int step = (hi - lo + 31) >> 5;
-      const int pos = lo + lane * step;
-      const unsigned m = __ballot_sync(FULL, pos < hi && wkey64()[pos] < k);
-      const int c = __popc(m);
-      const int nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
-      const int nhi = min(hi, lo + c * step);
-      lo = nlo;
-      hi = nhi;
+  // ---- trail_plus waiting set (policies.py:171-173 order: remaining, arrival, id) ----
+  // Bucket b holds the waiting requests with remaining output b as a list in id order
+  // (arrival order == id order: the trace is sorted, cluster.py:81-83); t_head[b] is its
+  // first id, w_rid[id] the next id, w_pend[id] the pending prefill | FLAG_SEEN. Level 0 of
+  // t_lv is each bucket's minimum block need, every level above the minimum of 32 children,
+  // so "first candidate in key order that could be admitted" is a few warp ballots
+  // (t_find) instead of a walk over the whole waiting set.
+  __device__ __forceinline__ int t_next(int id) const { return p.w_rid[id]; }
+  __device__ __forceinline__ int t_pend(int id) const { return p.w_pend[id]; }
+  __device__ void trail_init() {
+    for (int i = lane; i < cfg.tg.nb; i += 32) p.t_head[i] = -1;
+    for (int i = lane; i < cfg.tg.total; i += 32) p.t_lv[i] = 0x7fffffff;
+    __syncwarp();
+  }
+  // level offset without dynamic indexing (keeps Cfg in registers)
+  __device__ __forceinline__ int t_off(int l) const {
+    return l == 0 ? 0 : (l == 1 ? cfg.tg.off[1] : (l == 2 ? cfg.tg.off[2] : cfg.tg.off[3]));
+  }
+  // first bucket >= b0 whose minimum need is <= T, or -1
+  __device__ int t_find(int b0, int T) const {
+    if (b0 >= cfg.tg.nb) return -1;
+    int lvl = 0, idx = b0, node = -1;
+    while (true) {
+      const int base = idx & ~31;
+      const int v = p.t_lv[t_off(lvl) + base + lane];
+      const bool ok = v <= T && (lvl == 0 ? lane >= (idx & 31) : lane > (idx & 31));
+      const unsigned m = __ballot_sync(FULL, ok);
+      if (m) { node = base + __ffs(m) - 1; break; }
+      if (lvl == cfg.tg.top) return -1;
+      idx >>= 5;
+      lvl += 1;
     }
-    const int pos = lo + lane;
-    return lo + __popc(__ballot_sync(FULL, pos < hi && wkey64()[pos] < k));
+    while (lvl > 0) {  // descend: some child of a node <= T is <= T
+      lvl -= 1;
+      const int base = node << 5;
+      const unsigned m = __ballot_sync(FULL, p.t_lv[t_off(lvl) + base + lane] <= T);
+      node = base + __ffs(m) - 1;
+    }
+    return node;
+  }
+  // set bucket b's minimum and restore "node = min of children" up the tree
+  __device__ void t_set_leaf(int b, int val) {
+    if (p.t_lv[b] == val) return;
+    __syncwarp();
+    if (lane == 0) p.t_lv[b] = val;
+    __syncwarp();
+    int idx = b;
+    for (int l = 1; l <= cfg.tg.top; ++l) {
+      const int parent = idx >> 5;
+      const int mn = __reduce_min_sync(FULL, p.t_lv[t_off(l - 1) + (parent << 5) + lane]);
+      const int at = t_off(l) + parent;
+      if (p.t_lv[at] == mn) break;
+      __syncwarp();
+      if (lane == 0) p.t_lv[at] = mn;
+      __syncwarp();
+      idx = parent;
+    }
   }
   __device__ void trail_insert(int rid_flag, int pend, int rem) {
-    const unsigned long long k = ((unsigned long long)(unsigned)rem << 32) | (unsigned)(rid_flag & 0x7fffffff);
-    const int n = st.W;
-    if (n + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; return; }
-    const int pos = trail_lower_bound(k, n);
-    for (int hi = n; hi > pos; hi -= 32) {  // shift [pos, n) up one slot, top chunk first
-      const int lo = max(pos, hi - 32);
-      const int i = lo + lane;
-      const bool v = i < hi;
-      unsigned long long kk = 0;
-      int r = 0, pd = 0;
-      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
-      __syncwarp();
-      if (v) { wkey64()[i + 1] = kk; p.w_rid[i + 1] = r; p.w_pend[i + 1] = pd; }
-      __syncwarp();
-    }
-    if (lane == 0) { wkey64()[pos] = k; p.w_rid[pos] = rid_flag; p.w_pend[pos] = pend; }
+    const int id = rid_flag & 0x7fffffff;
+    int prev = -1, cur = p.t_head[rem];
+    while (cur >= 0 && cur < id) { prev = cur; cur = t_next(cur); }
     __syncwarp();
-    st.W = n + 1;
+    if (lane == 0) {
+      p.w_rid[id] = cur;
+      p.w_pend[id] = pend | (rid_flag & FLAG_SEEN);
+      if (prev < 0) p.t_head[rem] = id; else p.w_rid[prev] = id;
+    }
+    __syncwarp();
+    const int need = blocks(pend);
+    if (need < p.t_lv[rem]) t_set_leaf(rem, need);
+    st.W += 1;
   }
-  __device__ void trail_remove(int pos) {  // shift (pos, W) down one slot
-    for (int lo = pos + 1; lo < st.W; lo += 32) {
-      const int i = lo + lane;
-      const bool v = i < st.W;
-      unsigned long long kk = 0;
-      int r = 0, pd = 0;
-      if (v) { kk = wkey64()[i]; r = p.w_rid[i]; pd = p.w_pend[i]; }
-      __syncwarp();
-      if (v) { wkey64()[i - 1] = kk; p.w_rid[i - 1] = r; p.w_pend[i - 1] = pd; }
-      __syncwarp();
+  // unlink `cur` (predecessor `prev`, -1 = head) from bucket b; `need` = its block need
+  __device__ void trail_remove(int b, int prev, int cur, int need) {
+    const int nx = t_next(cur);
+    __syncwarp();
+    if (lane == 0) { if (prev < 0) p.t_head[b] = nx; else p.w_rid[prev] = nx; }
+    __syncwarp();
+    if (need == p.t_lv[b]) {  // it may have been the minimum: recompute the bucket's
+      int mn = 0x7fffffff;
+      for (int c = p.t_head[b]; c >= 0; c = t_next(c)) mn = min(mn, blocks(t_pend(c) & 0x7fffffff));
+      t_set_leaf(b, mn);
     }
     st.W -= 1;
   }
@@ -689,190 +713,150 @@ struct Eng {
     return nd;
   }
 
-  // ---- trail_plus victims: eligible running entries sorted by (-remaining, -dispatch_seq) ----
-  // eligible = unmarked (r_plan == 0) and generated < c * output_len (policies.py:190-196).
-  // Compact 64-bit keys (remaining << 32 | table index) -> rank sort -> prefix block sums.
-  __device__ __forceinline__ bool victim_eligible(int j, int& g, int& o) const {
-    if (p.r_plan[j] != 0) return false;
-    g = p.r_gen[j];
-    o = p.r_out[j];
-    return (double)g < __dmul_rn(cfg.c, (double)o);
-  }
-  __device__ int build_victims() {
+  // ---- trail_plus victims (policies.py:190-204) ----
+  // Eligible running entries (generated < c * output_len) as an unsorted set of 64-bit keys
+  // (remaining << 32 | table index) + allocated blocks: lane v holds victim v when V <= 32,
+  // else the set lives in v_key / v_cum. G(b) (blocks of unmarked victims with remaining > b)
+  // is one REDUX per 32 victims; the victims a covered candidate takes are extracted in key
+  // order (largest remaining first, youngest dispatch first on ties, :197) by warp argmax.
+  // A taken (marked) victim's key becomes 0, which no later query or extraction matches.
+  __device__ int victims_build(unsigned long long& vk, int& vb) {
     int V = 0;
     for (int base = 0; base < st.R; base += 32) {
       const int j = base + lane;
-      int g = 0, o = 0;
-      const bool e = j < st.R && victim_eligible(j, g, o);
+      bool e = false;
+      unsigned long long key = 0;
+      int blk = 0;
+      if (j < st.R) {
+        const int g = p.r_gen[j], o = p.r_out[j];
+        e = (double)g < __dmul_rn(cfg.c, (double)o);
+        key = ((unsigned long long)(unsigned)(o - g) << 32) | (unsigned)j;
+        blk = blocks(p.r_prompt[j] + g);
+      }
       const unsigned m = __ballot_sync(FULL, e);
-      if (e) p.v_key[V + __popc(m & lanemask_lt())] = ((unsigned long long)(unsigned)(o - g) << 32) | (unsigned)j;
+      if (e) {
+        const int d = V + __popc(m & lanemask_lt());
+        p.v_key[d] = key;
+        p.v_cum[d] = blk;
+      }
       V += __popc(m);
     }
     __syncwarp();
-    // descending key == (-remaining, -dispatch_seq)
-    if (V <= 32) {  // rank sort in registers: V shuffle steps (V is usually a handful)
-      const unsigned long long k = lane < V ? p.v_key[lane] : 0ULL;
-      int rank = 0;
-#pragma unroll 1
-      for (int u = 0; u < V; ++u) rank += __shfl_sync(FULL, k, u) > k;
-      if (lane < V) victims_write(k, rank, V);
-#ifdef SSB_SORT256
-    } else if (V <= 256) {
-      sort_keys_desc_256(p.v_key, V);
-      for (int i = lane; i < V; i += 32) victims_write(p.v_key[i], i, V);
-#endif
-    } else {
-      for (int i = lane; i < V; i += 32) {  // larger victim sets: rank sort in shared memory
-        const unsigned long long k = p.v_key[i];
-        int rank = 0;
-#pragma unroll 1
-        for (int u = 0; u < V; ++u) rank += p.v_key[u] > k;
-        victims_write(k, rank, V);
-      }
-    }
-    __syncwarp();
-    int carry = 0;  // prefix block sums (<= pool blocks: fits 32 bits)
-    for (int base = 0; base < V; base += 32) {
-      const int i = base + lane;
-      const int b = i < V ? (int)p.v_cum[i] : 0;
-      const int incl = warp_incl_scan(b, lane) + carry;
-      if (i < V) p.v_cum[i] = incl;
-      carry = __shfl_sync(FULL, incl, 31);
-    }
-    __syncwarp();
+    vk = lane < V ? p.v_key[lane] : 0ULL;
+    vb = lane < V ? (int)p.v_cum[lane] : 0;
     return V;
   }
-  __device__ __forceinline__ void victims_write(unsigned long long k, int rank, int V) {
-    if (rank < V) {
-      const int j = (int)(unsigned)k;
-      p.v_idx[rank] = j;
-      p.v_rem[rank] = (int)(k >> 32);
-      p.v_cum[rank] = blocks(p.r_prompt[j] + p.r_gen[j]);
-    }
-  }
-  // Σ allocated blocks over eligible victims: an upper bound of any candidate's gain
-  __device__ long long victims_total() const {
+  __device__ __forceinline__ long long victims_gain(int V, unsigned long long vk, int vb, int b) const {
+    if (V <= 32) return redux_add((int)(vk >> 32) > b ? vb : 0);
     long long t = 0;
-    for (int base = 0; base < st.R; base += 32) {
-      const int j = base + lane;
-      int g = 0, o = 0;
-      const bool e = j < st.R && victim_eligible(j, g, o);
-      t += redux_add(e ? blocks(p.r_prompt[j] + g) : 0);
+    for (int base = 0; base < V; base += 32) {
+      const int i = base + lane;
+      const unsigned long long k = i < V ? p.v_key[i] : 0ULL;
+      t += redux_add((int)(k >> 32) > b ? (int)p.v_cum[i] : 0);
     }
     return t;
   }
-  // number of victims with remaining > r (a prefix of the sorted list)
-  __device__ __forceinline__ int victims_above(int V, int r) const {
-    int lo = 0, hi = V;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (p.v_rem[mid] > r) lo = mid + 1; else hi = mid;
+  // mark the top victim with remaining > b; returns its blocks, table index in j_out
+  __device__ int victims_take(int V, unsigned long long& vk, int& vb, int b, int& j_out) {
+    if (V <= 32) {
+      const unsigned w = warp_argmax_u64(vk, (int)(vk >> 32) > b);
+      const int wl = __ffs(w) - 1;
+      j_out = (int)(unsigned)__shfl_sync(FULL, vk, wl);
+      const int blk = __shfl_sync(FULL, vb, wl);
+      if (lane == wl) vk = 0ULL;
+      return blk;
     }
-    return lo;
+    unsigned long long best = 0;
+    int bpos = -1;
+    for (int i = lane; i < V; i += 32) {
+      const unsigned long long k = p.v_key[i];
+      if ((int)(k >> 32) > b && k > best) { best = k; bpos = i; }
+    }
+    const unsigned w = warp_argmax_u64(best, bpos >= 0);
+    const int wl = __ffs(w) - 1;
+    const int pos = __shfl_sync(FULL, bpos, wl);
+    j_out = (int)(unsigned)__shfl_sync(FULL, best, wl);
+    const int blk = (int)p.v_cum[pos];
+    __syncwarp();
+    if (lane == 0) p.v_key[pos] = 0ULL;
+    __syncwarp();
+    return blk;
   }
 
   // ---- trail_plus (policies.py:168-212): greedy skip in (remaining, arrival, id) order ----
-  // arrival order == id order (trace sorted, ids in trace order), so the key is (remaining, id)
-  // and the waiting set is kept sorted by it. The walk visits 32 candidates per step: a
-  // candidate is actionable if it fits the free pool or (c > 0) the victims can cover it;
-  // the first actionable one is taken (dispatch, possibly after choosing victims), removed
-  // from the set, and the walk resumes at the same slot with the updated free pool/marks.
-  // Victims are only sorted when a blocked candidate passes the cheap upper bound
-  // need <= free + Σ(eligible blocks). Dispatches go to l_a (rid|flag) / l_c (pending).
+  // A candidate is admitted iff need <= free + G(remaining): with need <= free it is a plain
+  // dispatch (:183-186), else the victims taken largest-remaining-first cover it (:189-206).
+  // G is non-increasing in the remaining output, so free + G(b) bounds every candidate in
+  // buckets >= b and t_find skips every bucket whose minimum need exceeds it; a found bucket
+  // is checked against its exact threshold free + G(bucket) before its list is walked.
+  // Dispatches go to l_a (rid|flag) / l_c (pending), preempts to l_b.
   __device__ void select_trail(int& nd_out, int& np_out) {
     int nd = 0, np = 0;
     if (st.W == 0) { nd_out = np_out = 0; return; }
-    const bool can_preempt = cfg.c != 0.0;
-    if (can_preempt)
-      for (int j = lane; j < st.R; j += 32) p.r_plan[j] = 0;  // marks
-    __syncwarp();
+    int V = 0;
+    unsigned long long vk = 0;
+    int vb = 0;
+    if (cfg.c != 0.0) V = victims_build(vk, vb);
     int free = st.free_blocks;
-    int V = -1;
-    int vr = 0x7fffffff;  // victims held in registers when V <= 32: lane v has (remaining, cumulative blocks)
-    long long vc = 0;
-    int k0 = 0;
-    while (k0 < st.W) {
-      if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;
-      const int k = k0 + lane;
-      const bool v = k < st.W;
-      unsigned long long key = 0;
-      int pend = 0, need = 0;
-      if (v) { key = wkey64()[k]; pend = p.w_pend[k]; need = blocks(pend); }
-      const int rem = (int)(key >> 32);
-      const bool fit = v && need <= free;
-      const unsigned mfit = __ballot_sync(FULL, fit);
-      const int ffit = mfit ? __ffs(mfit) - 1 : 32;
-      int act = ffit;
-      if (can_preempt && ffit > 0) {
-        if (V < 0) {
-          V = build_victims();
-          vr = lane < V ? p.v_rem[lane] : -1;
-          vc = lane < V ? p.v_cum[lane] : 0;
-        }
-        // G(rem) = blocks of eligible victims with remaining > rem: non-increasing in rem, and the
-        // chunk's candidates are in ascending rem, so G(first candidate) bounds the whole chunk
-        const int rem0 = __shfl_sync(FULL, rem, 0);
-        long long g0;
-        if (V <= 32) {
-          const int m0 = __popc(__ballot_sync(FULL, vr > rem0));
-          g0 = m0 > 0 ? __shfl_sync(FULL, vc, m0 - 1) : 0;
-        } else {
-          const int m0 = victims_above(V, rem0);
-          g0 = m0 > 0 ? p.v_cum[m0 - 1] : 0;
-        }
-        const bool maybe = v && !fit && lane < ffit && (long long)need <= (long long)free + g0;
-        if (__any_sync(FULL, maybe)) {
-          long long gain;
-          if (V <= 32) {
-            int m = 0;
-#pragma unroll 1
-            for (int u = 0; u < V; ++u) m += __shfl_sync(FULL, vr, u) > rem;
-            gain = __shfl_sync(FULL, vc, m > 0 ? m - 1 : 0);
-            if (m == 0) gain = 0;
-          } else {
-            const int m = maybe ? victims_above(V, rem) : 0;
-            gain = m > 0 ? p.v_cum[m - 1] : 0;
-          }
-          const unsigned mcov = __ballot_sync(FULL, maybe && (long long)free + gain >= need);
-          if (mcov) act = __ffs(mcov) - 1;
+    int b = 0, after = -1;  // resume point: bucket b, ids > after
+    while (true) {
+      if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;  // :179-181
+      long long T = (long long)free + (V > 0 ? victims_gain(V, vk, vb, b) : 0);
+      if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
+      const int fb = t_find(b, (int)T);
+#ifdef SSB_PHASE_TIMING
+      tc[6] += 1;
+#endif
+      if (fb < 0) break;
+      if (fb != b) {
+        b = fb;
+        after = -1;
+        if (V > 0) {  // exact threshold of the found bucket
+          T = (long long)free + victims_gain(V, vk, vb, b);
+          if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
+          if (p.t_lv[b] > T) { b += 1; continue; }
         }
       }
-      if (act == 32) { k0 += 32; continue; }
-      const int cpos = k0 + act;
-      const int crem = __shfl_sync(FULL, rem, act);
-      const int cpend = __shfl_sync(FULL, pend, act);
-      const int cneed = blocks(cpend);
-      const int rid_flag = p.w_rid[cpos];
-      if (cneed > free) {
+      int prev = -1, cur = p.t_head[b], pv = 0, need = 0;
+      while (cur >= 0 && cur <= after) { prev = cur; cur = t_next(cur); }
+      while (cur >= 0) {
+#ifdef SSB_PHASE_TIMING
+        tm[6] += 1;
+#endif
+        pv = t_pend(cur);
+        need = blocks(pv & 0x7fffffff);
+        if ((long long)need <= T) break;
+        prev = cur;
+        cur = t_next(cur);
+      }
+      if (cur < 0) { b += 1; after = -1; continue; }
+      if (need > free) {
         // take victims (largest remaining first, youngest first on ties) until free+gain >= need
-        const int m = victims_above(V, crem);
-        long long gain = 0;
-        int taken = 0;
-        while (taken < m && (long long)free + gain < cneed) {
-          gain = p.v_cum[taken];
-          taken++;
+        int gain = 0;
+        while (free + gain < need) {
+          int j;
+          gain += victims_take(V, vk, vb, b, j);
+          if (lane == 0) p.l_b[np] = j;
+          np++;
         }
-        for (int t = lane; t < taken; t += 32) {
-          const int j = p.v_idx[t];
-          p.r_plan[j] = 1;  // marked
-          p.l_b[np + t] = j;
-        }
-        np += taken;
-        free += (int)gain;
-        V = -1;  // marks changed: rebuild before the next coverability check
+        free += gain;
         __syncwarp();
       }
-      if (lane == 0) { p.l_a[nd] = rid_flag; p.l_c[nd] = cpend; }
+      if (lane == 0) { p.l_a[nd] = cur | (pv & FLAG_SEEN); p.l_c[nd] = pv & 0x7fffffff; }
+#ifdef SSB_PHASE_TIMING
+      tc[7] += 1;
+#endif
       nd++;
-      free -= cneed;
+      free -= need;
       __syncwarp();
-      trail_remove(cpos);  // the next candidate moves into slot cpos
-      k0 = cpos;
+      trail_remove(b, prev, cur, need);
+      after = cur;
     }
     __syncwarp();
     nd_out = nd;
     np_out = np;
   }
+
 
   // ---- remove dispatched entries (physical slots in l_a[0..nd)) from an unordered waiting set ----
   __device__ void remove_dispatched_unordered(int nd) {

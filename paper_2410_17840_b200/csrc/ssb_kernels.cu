@@ -27,10 +27,11 @@ __host__ __device__ inline long long align_up(long long x, long long a) { return
 
 struct Layout {
   long long srv, w_enq, w_rid, w_pend, w_key, r_rid, r_prompt, r_out, r_gen, r_pfd, r_st, r_plan, l_a, l_b, v_idx,
-      v_rem, v_cum, v_key, l_c, rl, total;
+      v_rem, v_cum, v_key, l_c, rl, t_head, t_lv, total;
 };
 
-__host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers, int policy) {
+__host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long long N, int n_servers,
+                                              const ssb_engine_params& e) {
   Layout L;
   long long o = 0;
   L.srv = o;      o = align_up(o + (long long)sizeof(Srv), 64);
@@ -52,8 +53,11 @@ __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long l
   L.v_cum = o;    o = align_up(o + 8 * Rc, 64);
   L.v_key = o;    o = align_up(o + 8 * Rc, 64);
   L.l_c = o;      o = align_up(o + 4 * Rc, 64);
-  (void)policy;
   L.rl = o;       o = align_up(o + (n_servers > 1 ? 4 * N : 0), 64);
+  const bool trail = e.policy == SSB_POLICY_TRAIL_PLUS;
+  const TrailGeom tg = trail_geom(e.max_context, e.pool_blocks, e.block_size);
+  L.t_head = o;   o = align_up(o + (trail ? 4LL * tg.nb : 0), 64);
+  L.t_lv = o;     o = align_up(o + (trail ? 4LL * tg.total : 0), 64);
   L.total = align_up(o, 256);
   return L;
 }
@@ -79,6 +83,8 @@ __device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
   p.v_key = (unsigned long long*)(base + L.v_key);
   p.l_c = (int*)(base + L.l_c);
   p.rl = (int*)(base + L.rl);
+  p.t_head = (int*)(base + L.t_head);
+  p.t_lv = (int*)(base + L.t_lv);
   return p;
 }
 
@@ -103,6 +109,7 @@ __device__ inline Cfg make_cfg(const ssb_instance& I) {
   c.compute = e.compute_per_token_s;
   c.overhead = e.overhead_s;
   c.qps = I.qps_factor;
+  c.tg = trail_geom(e.max_context, e.pool_blocks, e.block_size);
   return c;
 }
 
@@ -194,12 +201,13 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
   const long long t0 = clock64();
   const ssb_instance I = inst[idx];
   const Cfg cfg = make_cfg(I);
-  const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine.policy);
+  const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
   Eng E;
   bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap, sm_tab);
   clear_records(E, I.n_requests, lane, 32);
   fill_events(E, lane, 32);
   init_srv(E.st, cfg);
+  if (cfg.policy == SSB_POLICY_TRAIL_PLUS) E.trail_init();
   __syncwarp();
   E.advance(__longlong_as_double(0x7ff0000000000000LL), (int)I.n_requests);  // t_lim = +inf
   if (E.st.status == SSB_OK && (E.st.finished != I.n_requests || E.has_work())) E.st.status = SSB_E_INVARIANT;
@@ -342,7 +350,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   const bool tabs_in_smem = smem_tabs != 0;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
   const Cfg cfg = make_cfg(I);
-  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine.policy);
+  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
 
   // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
@@ -350,6 +358,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
     Eng E;
     bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tabs_in_smem ? sm_tabs + s * SM_COLS * RS : nullptr);
     init_srv(E.st, cfg);
+    if (cfg.policy == SSB_POLICY_TRAIL_PLUS) E.trail_init();
     fill_events(E, lane, 32);
     if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
   }
@@ -574,7 +583,7 @@ extern "C" size_t ssb_prepare(ssb_instance* h, int32_t n_inst) {
     I.wait_cap = (int32_t)Wc;
     I.run_cap = (int32_t)Rc;
     I.scratch_offset = off;
-    Layout L = make_layout(Wc, Rc, N, I.n_servers, I.engine.policy);
+    Layout L = make_layout(Wc, Rc, N, I.n_servers, I.engine);
     off += L.total * (long long)std::max(1, I.n_servers);
   }
   return (size_t)off;
@@ -595,7 +604,10 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const ssb_instance& I = h_inst[i];
     if (I.n_servers < 1 || I.n_requests < 0 || I.n_requests > 0x7fffffffLL || I.wait_cap < 1 || I.run_cap < 1)
       return SSB_E_ARG;
-    Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine.policy);
+    if (I.engine.policy == SSB_POLICY_TRAIL_PLUS &&
+        std::min<long long>(I.engine.max_context, (long long)I.engine.pool_blocks * I.engine.block_size) >= (1LL << 20))
+      return SSB_E_ARG;  // remaining-output buckets: 4 tree levels (2^20 buckets) at most
+    Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
     need = std::max(need, I.scratch_offset + L.total * (long long)I.n_servers);
     if (I.n_servers == 1) singles.push_back(i); else { multis.push_back(i); max_servers = std::max(max_servers, I.n_servers); }
   }

@@ -44,6 +44,27 @@ print(f"samples {tot}, warp-instructions {totx}")
 src = {}
 for (f, n), c in agg.most_common(top):
     pass
+# per enclosing function (nearest preceding __device__/__global__ definition)
+import re as _re
+srcs = {}
+def func_of(f, n):
+    pth = next((q for q in ["paper_2410_17840_b200/csrc/" + f, "include/" + f] if os.path.exists(q)), None)
+    if not pth:
+        return f
+    L = srcs.setdefault(pth, open(pth).read().splitlines())
+    for i in range(n - 1, -1, -1):
+        m = _re.search(r'(?:__device__|__global__)[^(]*?\b(\w+)\s*\(', L[i])
+        if m:
+            return f"{f}:{m.group(1)}"
+    return f
+fs, fx = collections.Counter(), collections.Counter()
+for key in set(agg) | set(aggx):
+    fn = func_of(*key) if key else "?"
+    fs[fn] += agg[key]; fx[fn] += aggx[key]
+print("-- per function: stall samples, executed warp-instructions")
+for fn, c in fs.most_common(25):
+    print(f"{c:7d} {100*c/tot:5.1f}%  ex {fx[fn]:10d} {100*fx[fn]/max(totx,1):5.1f}%  {fn}")
+print("-- per line")
 for key, c in agg.most_common(top):
     if key is None:
         print(f"{c:7d} {100*c/tot:5.1f}%  ?"); continue

@@ -14,6 +14,8 @@ jobs = {"c1": lambda: C.c1_jobs()[:1], "c1l": lambda: C.c1_jobs()[1:], "c2s": la
         "c4trail": lambda: [j for j in C.c4_jobs() if j[3].split("/")[1] == "trail_plus"],
         "trailworst": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/trail_plus/1024/x4.0/s0"],
         "trailbig": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/trail_plus/11444/x4.0/s0"],
+        "npworst": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/nopreempt/1024/x4.0/s0"],
+        "sparse": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/larry/11444/x0.25/s0"],
         "larryworst": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/larry/1024/x4.0/s0"],
         "c4larry": lambda: [j for j in C.c4_jobs() if j[3].split("/")[1] == "larry"]}[which]()
 db = simulate.upload(I.make_batch(jobs))
