@@ -230,7 +230,8 @@ __device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restri
 
 struct Eng {
 #ifdef SSB_PHASE_TIMING
-  long long tm[8], tc[8];  // 0 enqueue 1 select 2 preempt+dispatch 3 fast 4 small 5 general 6/7 walk counters
+  long long tm[16], tc[16];  // 0 enqueue 1 select 2 preempt+dispatch 3 fast 4 small 5 general 6/7 walk counters
+                            // 8 victims_build 9 t_find 10 bucket walk 11 trail_remove 12 victims_take 13 preempts 14 small->general
 #endif
   Cfg cfg;
   Srv st;
@@ -796,14 +797,18 @@ struct Eng {
     int V = 0;
     unsigned long long vk = 0;
     int vb = 0;
+    SSB_T0(vb)
     if (cfg.c != 0.0) V = victims_build(vk, vb);
+    SSB_T1(vb, 8)
     int free = st.free_blocks;
     int b = 0, after = -1;  // resume point: bucket b, ids > after
     while (true) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;  // :179-181
       long long T = (long long)free + (V > 0 ? victims_gain(V, vk, vb, b) : 0);
       if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
+      SSB_T0(tf)
       const int fb = t_find(b, (int)T);
+      SSB_T1(tf, 9)
 #ifdef SSB_PHASE_TIMING
       tc[6] += 1;
 #endif
@@ -817,6 +822,7 @@ struct Eng {
           if (p.t_lv[b] > T) { b += 1; continue; }
         }
       }
+      SSB_T0(wk)
       int prev = -1, cur = p.t_head[b], pv = 0, need = 0;
       while (cur >= 0 && cur <= after) { prev = cur; cur = t_next(cur); }
       while (cur >= 0) {
@@ -829,8 +835,10 @@ struct Eng {
         prev = cur;
         cur = t_next(cur);
       }
+      SSB_T1(wk, 10)
       if (cur < 0) { b += 1; after = -1; continue; }
       if (need > free) {
+        SSB_T0(vt)
         // take victims (largest remaining first, youngest first on ties) until free+gain >= need
         int gain = 0;
         while (free + gain < need) {
@@ -841,6 +849,7 @@ struct Eng {
         }
         free += gain;
         __syncwarp();
+        SSB_T1(vt, 12)
       }
       if (lane == 0) { p.l_a[nd] = cur | (pv & FLAG_SEEN); p.l_c[nd] = pv & 0x7fffffff; }
 #ifdef SSB_PHASE_TIMING
@@ -849,7 +858,9 @@ struct Eng {
       nd++;
       free -= need;
       __syncwarp();
+      SSB_T0(rm)
       trail_remove(b, prev, cur, need);
+      SSB_T1(rm, 11)
       after = cur;
     }
     __syncwarp();
@@ -1225,6 +1236,9 @@ struct Eng {
       if (valid) p.r_plan[lane] = in_dec ? 1 : (in_pf ? chunk + 1 : 0);
       if (in_pf) p.l_b[__popc(m_pf & lt)] = lane;
       __syncwarp();
+#ifdef SSB_PHASE_TIMING
+      tc[14] += 1;
+#endif
       bool removed = progress(__popc(m_pf));
       if (removed) compact_running();
       if (total > st.peak) st.peak = total;
@@ -1354,6 +1368,7 @@ struct Eng {
     }
     SSB_T0(disp)
     if (np > 0) {  // policy preempts first (engine.py:203-204), in decision order
+      SSB_T0(pre)
       drop_regs();
       for (int t = 0; t < np; ++t) {
         int j = p.l_b[t];
@@ -1363,6 +1378,7 @@ struct Eng {
       }
       flush_pushes();
       compact_running();
+      SSB_T1(pre, 13)
     }
     if (nd > 0) {
       drop_regs();
@@ -1403,7 +1419,7 @@ struct Eng {
   }
   __device__ void advance(double t_lim, int n_avail) {
 #ifdef SSB_PHASE_TIMING
-    for (int i = 0; i < 8; ++i) tm[i] = tc[i] = 0;
+    for (int i = 0; i < 16; ++i) tm[i] = tc[i] = 0;
 #endif
     init_modes();
     double next_t = next_arrival(n_avail);
@@ -1432,6 +1448,9 @@ struct Eng {
     if (lane == 0)
       printf("PHASES iters %lld | enq %lld/%lld | sel %lld/%lld | disp %lld/%lld | fast %lld/%lld | small %lld/%lld | gen %lld/%lld | walk %lld/%lld | victims %lld/%lld\n",
              st.iterations, tm[0], tc[0], tm[1], tc[1], tm[2], tc[2], tm[3], tc[3], tm[4], tc[4], tm[5], tc[5], tm[6], tm[7], tc[6], tc[7]);
+    if (lane == 0)
+      printf("PHASES2 vbuild %lld/%lld | tfind %lld/%lld | walk %lld/%lld | remove %lld/%lld | vtake %lld/%lld | preempt %lld/%lld | small->gen %lld\n",
+             tm[8], tc[8], tm[9], tc[9], tm[10], tc[10], tm[11], tc[11], tm[12], tc[12], tm[13], tc[13], tc[14]);
 #endif
   }
 };

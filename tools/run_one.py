@@ -17,7 +17,12 @@ jobs = {"c1": lambda: C.c1_jobs()[:1], "c1l": lambda: C.c1_jobs()[1:], "c2s": la
         "npworst": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/nopreempt/1024/x4.0/s0"],
         "sparse": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/larry/11444/x0.25/s0"],
         "larryworst": lambda: [j for j in C.c4_jobs(seeds=range(1)) if j[3] == "C4/larry/1024/x4.0/s0"],
-        "c4larry": lambda: [j for j in C.c4_jobs() if j[3].split("/")[1] == "larry"]}[which]()
+        "c4larry": lambda: [j for j in C.c4_jobs() if j[3].split("/")[1] == "larry"]}.get(which)
+if jobs is None:  # a C4 label, e.g. C4/trail_plus/1024/x2.0/s7
+    seed = int(which.rsplit("/s", 1)[1])
+    jobs = [j for j in C.c4_jobs(seeds=[seed]) if j[3] == which]
+else:
+    jobs = jobs()
 db = simulate.upload(I.make_batch(jobs))
 for _ in range(reps):
     simulate.launch(db)
