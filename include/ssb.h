@@ -207,6 +207,24 @@ int32_t ssb_summarize(ssb_trace trace, ssb_records records,
                       int32_t n_groups, ssb_summary* d_summary,
                       void* d_work, size_t work_bytes, void* stream);
 
+/* Pooled percentiles (one metric set over the union of many groups, and across
+ * GPUs): pass `pass` (0..7) of an MSD radix select with 8-bit digits on the
+ * order-preserving 64-bit image of each metric value. For each of the 13 rank
+ * slots (TTFT p50/95/99, nTTFT p50/95, TGT p50/95, TPOT p50/95/99, queueing
+ * delay p50/95/99; same per-record metrics as ssb_summarize) with
+ * d_active[s] != 0, counts the records of ALL groups whose key matches
+ * d_prefix[s] in the bits above the pass's digit into d_hist[s*256 + digit]
+ * (zeroed by the call). Pass 0 also writes d_counts = {n, n_tpot,
+ * n_preempted}. d_work: >= 8*(n_groups+1) bytes. The host sums the
+ * histograms over ranks (one all-gather per pass) and extends the prefixes
+ * (paper_2410_17840_b200/pooled.py). Replaces summarize() (metrics.py:80-99)
+ * over concatenated record lists, without moving records between GPUs. */
+int32_t ssb_pool_hist(ssb_trace trace, ssb_records records,
+                      const ssb_summary_group* h_groups, const ssb_summary_group* d_groups,
+                      int32_t n_groups, const uint64_t* d_prefix, const int32_t* d_active,
+                      int32_t pass, uint32_t* d_hist, uint64_t* d_counts,
+                      void* d_work, size_t work_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -185,6 +185,24 @@ EXPORTS = {
             ctypes.c_void_p,
         ],
     ),
+    "ssb_pool_hist": (
+        ctypes.c_int32,
+        [
+            SsbTrace,
+            SsbRecords,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_int32,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_int32,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+            ctypes.c_size_t,
+            ctypes.c_void_p,
+        ],
+    ),
     "ssb_struct_sizes": (ctypes.c_int32, [ctypes.c_void_p]),
 }
 

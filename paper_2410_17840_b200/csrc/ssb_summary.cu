@@ -213,6 +213,73 @@ __global__ void k_finish(const ssb_summary_group* __restrict__ groups, int n_gro
   out[g] = S;
 }
 
+// Pooled histogram over ALL groups (one record set spread over many instances and,
+// across ranks, over many GPUs): the per-pass digit histogram of every rank slot whose
+// key matches that slot's current prefix, summed over the groups. The host all-gathers
+// these 13 x 256 counts across ranks and picks the digits (pooled.py), so an exact
+// nearest-rank percentile of the union of every rank's records costs 8 small
+// collectives and no record movement.
+__global__ void __launch_bounds__(THREADS) k_pool_hist(ssb_trace tr, ssb_records rec,
+                                                       const ssb_summary_group* __restrict__ groups, int n_groups,
+                                                       const long long* __restrict__ cstart, long long n_chunks,
+                                                       const unsigned long long* __restrict__ prefix,
+                                                       const int* __restrict__ active, int pass,
+                                                       unsigned* __restrict__ out_hist,
+                                                       unsigned long long* __restrict__ out_counts) {
+  __shared__ unsigned hist[NSLOT][256];
+  __shared__ unsigned long long s_prefix[NSLOT];
+  __shared__ int s_active[NSLOT];
+  const int shift = 56 - 8 * pass;
+  const unsigned long long hmask = pass == 0 ? 0ULL : (~0ULL << (shift + 8));
+  for (int i = threadIdx.x; i < NSLOT * 256; i += blockDim.x) (&hist[0][0])[i] = 0u;
+  if (threadIdx.x < NSLOT) {
+    s_prefix[threadIdx.x] = prefix[threadIdx.x] & hmask;
+    s_active[threadIdx.x] = active[threadIdx.x];
+  }
+  __syncthreads();
+  unsigned long long n_all = 0, n_tpot = 0, n_pre = 0;
+  for (long long c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const int g = find_group(cstart, n_groups, c);
+    const ssb_summary_group G = groups[g];
+    const long long e0 = (c - cstart[g]) * CHUNK;
+    const long long e1 = (e0 + CHUNK < G.n) ? e0 + CHUNK : G.n;
+    for (long long i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
+      unsigned long long key[5];
+      bool has_tpot;
+      element_keys(G, tr, rec, i, key, has_tpot);
+      if (pass == 0) {
+        n_all += 1;
+        n_tpot += has_tpot;
+        n_pre += rec.preempt_count[G.record_offset + i] > 0;
+      }
+#pragma unroll
+      for (int s = 0; s < NSLOT; ++s) {
+        const int st = SLOT_STAT[s];
+        if (!s_active[s] || (st == 3 && !has_tpot)) continue;
+        if ((key[st] & hmask) != s_prefix[s]) continue;
+        atomicAdd(&hist[s][(unsigned)(key[st] >> shift) & 255u], 1u);
+      }
+    }
+  }
+  if (pass == 0) {
+    for (int o = 16; o; o >>= 1) {
+      n_all += __shfl_xor_sync(0xffffffffu, n_all, o);
+      n_tpot += __shfl_xor_sync(0xffffffffu, n_tpot, o);
+      n_pre += __shfl_xor_sync(0xffffffffu, n_pre, o);
+    }
+    if ((threadIdx.x & 31) == 0 && n_all) {
+      atomicAdd(&out_counts[0], n_all);
+      atomicAdd(&out_counts[1], n_tpot);
+      atomicAdd(&out_counts[2], n_pre);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NSLOT * 256; i += blockDim.x) {
+    const unsigned v = (&hist[0][0])[i];
+    if (v) atomicAdd(&out_hist[i], v);
+  }
+}
+
 long long chunks_of(long long n) { return n > 0 ? (n + CHUNK - 1) / CHUNK : 0; }
 
 }  // namespace
@@ -250,5 +317,36 @@ extern "C" int32_t ssb_summarize(ssb_trace trace, ssb_records records, const ssb
     k_select<<<sel_grid, 256, 0, stream>>>(d_groups, n_groups, work, pass);
   }
   k_finish<<<(n_groups + 127) / 128, 128, 0, stream>>>(d_groups, n_groups, work, d_summary);
+  return cudaGetLastError() == cudaSuccess ? SSB_OK : SSB_E_CUDA;
+}
+
+extern "C" int32_t ssb_pool_hist(ssb_trace trace, ssb_records records, const ssb_summary_group* h_groups,
+                                 const ssb_summary_group* d_groups, int32_t n_groups, const uint64_t* d_prefix,
+                                 const int32_t* d_active, int32_t pass, uint32_t* d_hist, uint64_t* d_counts,
+                                 void* d_work, size_t work_bytes, void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (n_groups <= 0) return SSB_OK;
+  if (!h_groups || !d_groups || !d_prefix || !d_active || !d_hist || !d_counts || !d_work) return SSB_E_ARG;
+  if (pass < 0 || pass > 7 || work_bytes < sizeof(long long) * (size_t)(n_groups + 1)) return SSB_E_ARG;
+  std::vector<long long> cstart(n_groups + 1, 0);
+  for (int g = 0; g < n_groups; ++g) {
+    if (h_groups[g].n < 0) return SSB_E_ARG;
+    cstart[g + 1] = cstart[g] + chunks_of(h_groups[g].n);
+  }
+  const long long n_chunks = cstart[n_groups];
+  long long* d_cstart = (long long*)d_work;
+  if (cudaMemcpyAsync(d_cstart, cstart.data(), sizeof(long long) * cstart.size(), cudaMemcpyHostToDevice, stream) !=
+      cudaSuccess)
+    return SSB_E_CUDA;
+  if (cudaMemsetAsync(d_hist, 0, sizeof(uint32_t) * NSLOT * 256, stream) != cudaSuccess) return SSB_E_CUDA;
+  if (pass == 0 && cudaMemsetAsync(d_counts, 0, sizeof(uint64_t) * 3, stream) != cudaSuccess) return SSB_E_CUDA;
+  if (n_chunks == 0) return SSB_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<long long>(n_chunks, 4L * sms);
+  k_pool_hist<<<grid, THREADS, 0, stream>>>(trace, records, d_groups, n_groups, d_cstart, n_chunks,
+                                           (const unsigned long long*)d_prefix, d_active, pass, d_hist,
+                                           (unsigned long long*)d_counts);
   return cudaGetLastError() == cudaSuccess ? SSB_OK : SSB_E_CUDA;
 }

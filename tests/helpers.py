@@ -131,3 +131,39 @@ def compare_instance(sc, golden, batch, i, rec, stats, *, check_summary=None) ->
 
 
 __all__ = ["load_golden", "scenario_batch", "scenario_trace", "compare_instance", "fold_digests"]
+
+
+def pooled_host_values(batch, rec):
+    """Per-record metric arrays of every instance of `batch` concatenated (numpy,
+    the reference's operation order), plus the preempt counts — the pooled set."""
+    from paper_2410_17840_b200.pooled import metric_values
+
+    cols = {k: [] for k in ("arrival", "prompt", "output", "first_token", "finish", "first_dispatch", "pc")}
+    for inst in batch.instances:
+        o, t, n, f = int(inst["record_offset"]), int(inst["trace_offset"]), int(inst["n_requests"]), float(inst["qps_factor"])
+        cols["arrival"].append(batch.trace.arrival[t:t + n] / f)
+        cols["prompt"].append(batch.trace.prompt[t:t + n])
+        cols["output"].append(batch.trace.output[t:t + n])
+        cols["first_token"].append(rec.first_token[o:o + n])
+        cols["finish"].append(rec.finish[o:o + n])
+        cols["first_dispatch"].append(rec.first_dispatch[o:o + n])
+        cols["pc"].append(rec.preempt_count[o:o + n])
+    c = {k: np.concatenate(v) for k, v in cols.items()}
+    vals = metric_values(c["arrival"], c["prompt"], c["output"], c["first_token"], c["finish"], c["first_dispatch"])
+    return vals, c["pc"]
+
+
+def pooled_expected(vals, pc):
+    """sorted(union)[ceil(p/100*n)-1] per slot (metrics.py:46-54) + counts."""
+    import math
+
+    from paper_2410_17840_b200.pooled import SLOTS
+
+    out = {}
+    for metric, p in SLOTS:
+        v = np.sort(vals[metric], kind="stable")
+        out[f"{metric}_p{p}"] = float(v[math.ceil(p / 100 * len(v)) - 1]) if len(v) else float("nan")
+    n = len(vals["ttft"])
+    out.update(n_requests=n, n_tpot=len(vals["tpot"]), n_preempted=int((pc > 0).sum()),
+               preemption_rate=int((pc > 0).sum()) / n)
+    return out

@@ -135,3 +135,32 @@ def test_acceptance_criterion_4_direction():
     win50 = sum(by[(s, "larry")].ttft_p50 < by[(s, "fcfs")].ttft_p50 for s in range(1000, 1050))
     win95n = sum(by[(s, "larry")].norm_ttft_p95 < by[(s, "fcfs")].norm_ttft_p95 for s in range(1000, 1050))
     assert win50 >= 45 and win95n >= 40, (win50, win95n)
+
+
+def test_pooled_percentiles_on_device_match_sorted_union():
+    """ssb_pool_hist radix select over a multi-instance batch (C5 shape in miniature:
+    several seeds of a 16-replica SAL cluster + single engines with scale_qps) ==
+    sorted(concatenated records)[ceil(p/100*n)-1]."""
+    import torch
+
+    from helpers import pooled_expected, pooled_host_values
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200 import simulate
+    from paper_2410_17840_b200.pooled import pooled_summary_device
+
+    jobs = []
+    for seed in range(3):
+        tr = P.synthesize(P.SynthSpec(duration_s=30.0, mean_qps=40.0, burstiness=3.0, seed=seed))
+        jobs.append((P.ClusterSettings(16, P.EngineSettings(policy="larry"), P.BalancerSettings("sal"), seed), tr, 1.0))
+        jobs.append((P.ClusterSettings(1, P.EngineSettings(policy="trail_plus", c=0.5, pool_blocks=700),
+                                       P.BalancerSettings("rr"), seed), tr, 0.25))
+    batch = I.make_batch(jobs)
+    db = simulate.upload(batch)
+    simulate.launch(db)
+    torch.cuda.synchronize()
+    rec, st = simulate.download(db)
+    assert (st["status"] == 0).all()
+    got = pooled_summary_device(db)
+    want = pooled_expected(*pooled_host_values(batch, rec))
+    for k, v in want.items():
+        assert got[k] == v or (v != v and got[k] != got[k]), (k, got[k], v)
