@@ -98,7 +98,9 @@ typedef struct {
  * engine unless SSB_FLAG_GLOBAL_TABLES is set (then global, sized run_cap).
  * An instance that outgrows the shared table ends with SSB_E_CAPACITY and is
  * simply re-run with the flag (the host shim does this automatically). */
+#ifndef SSB_SMEM_RUN_CAP
 #define SSB_SMEM_RUN_CAP 256
+#endif
 #define SSB_FLAG_GLOBAL_TABLES 1
 
 /* Trace SoA, TraceEntry (workload.py:42-56); arrivals sorted per instance. */

@@ -40,13 +40,17 @@ constexpr unsigned long long FNV_PRIME = 0x100000001b3ULL;
 
 // trail_plus waiting set geometry: one bucket per remaining-output value
 // (remaining <= output_len < min(max_context, pool tokens), policies.py:56-68 feasibility),
-// a min-need tree over the buckets with fan-out 32 (one warp ballot per level).
-// Level l holds n_l = ceil(n_{l-1}/32) nodes, padded to a multiple of 32; the top level
-// fits one warp (<= 32 nodes).
+// a min-need tree over the buckets with fan-out 128: a warp reads one 128-node chunk as
+// one int4 per lane and finds the first qualifying node with one ballot, so a search is
+// at most 2 x levels dependent loads (2 levels up to 16,384 buckets, 3 up to 2^21).
+// Level l holds n_l = ceil(n_{l-1}/128) nodes, padded to a multiple of 128; the top level
+// is one chunk (<= 128 nodes).
+constexpr int TF = 128;       // fan-out
+constexpr int TF_SHIFT = 7;
 struct TrailGeom {
-  int nb;      // buckets (multiple of 32)
-  int top;     // index of the top level (0..3)
-  int off[4];  // level offsets (ints) into the level array
+  int nb;      // buckets (multiple of 128)
+  int top;     // index of the top level (0..2)
+  int off[4];  // level offsets (ints) into the level array (multiples of 128)
   int total;   // ints in the level array
 };
 __host__ __device__ inline TrailGeom trail_geom(int max_ctx, int pool, int bs) {
@@ -54,16 +58,16 @@ __host__ __device__ inline TrailGeom trail_geom(int max_ctx, int pool, int bs) {
   if ((long long)max_ctx < maxrem) maxrem = max_ctx;
   if (maxrem < 1) maxrem = 1;
   TrailGeom g;
-  long long n = (maxrem + 32) / 32 * 32;  // buckets 0..maxrem
-  if (n > (1LL << 20)) n = 1LL << 20;     // 4 levels at most (ssb_simulate rejects larger)
+  long long n = (maxrem + TF) / TF * TF;  // buckets 0..maxrem
+  if (n > (1LL << 20)) n = 1LL << 20;     // ssb_simulate rejects larger
   g.nb = (int)n;
   g.top = 0;
   g.off[0] = 0;
   g.off[1] = g.off[2] = g.off[3] = 0;
   long long o = n;
-  while (n > 32 && g.top < 3) {
-    n = (n + 31) / 32;
-    n = (n + 31) / 32 * 32;
+  while (n > TF && g.top < 2) {
+    n = (n + TF - 1) / TF;
+    n = (n + TF - 1) / TF * TF;
     g.top += 1;
     g.off[g.top] = (int)o;
     o += n;
@@ -373,27 +377,37 @@ struct Eng {
   }
   // level offset without dynamic indexing (keeps Cfg in registers)
   __device__ __forceinline__ int t_off(int l) const {
-    return l == 0 ? 0 : (l == 1 ? cfg.tg.off[1] : (l == 2 ? cfg.tg.off[2] : cfg.tg.off[3]));
+    return l == 0 ? 0 : (l == 1 ? cfg.tg.off[1] : cfg.tg.off[2]);
+  }
+  // first node of the 128-node chunk at `chunk` (int offset) with value <= T and index >= lo
+  // (chunk-relative), or -1: lane i holds nodes 4i..4i+3
+  __device__ __forceinline__ int t_chunk_first(int chunk, int lo, int T) const {
+    const int4 v = *reinterpret_cast<const int4*>(p.t_lv + chunk + 4 * lane);
+    const int q = 4 * lane;
+    const unsigned bits = (unsigned)(v.x <= T && q >= lo) | ((unsigned)(v.y <= T && q + 1 >= lo) << 1) |
+                          ((unsigned)(v.z <= T && q + 2 >= lo) << 2) | ((unsigned)(v.w <= T && q + 3 >= lo) << 3);
+    const unsigned m = __ballot_sync(FULL, bits != 0u);
+    if (m == 0u) return -1;
+    const int f = __ffs(m) - 1;
+    const unsigned fb = __shfl_sync(FULL, bits, f);
+    return 4 * f + __ffs(fb) - 1;
   }
   // first bucket >= b0 whose minimum need is <= T, or -1
   __device__ int t_find(int b0, int T) const {
     if (b0 >= cfg.tg.nb) return -1;
     int lvl = 0, idx = b0, node = -1;
     while (true) {
-      const int base = idx & ~31;
-      const int v = p.t_lv[t_off(lvl) + base + lane];
-      const bool ok = v <= T && (lvl == 0 ? lane >= (idx & 31) : lane > (idx & 31));
-      const unsigned m = __ballot_sync(FULL, ok);
-      if (m) { node = base + __ffs(m) - 1; break; }
+      const int base = idx & ~(TF - 1);
+      const int r = t_chunk_first(t_off(lvl) + base, lvl == 0 ? (idx & (TF - 1)) : (idx & (TF - 1)) + 1, T);
+      if (r >= 0) { node = base + r; break; }
       if (lvl == cfg.tg.top) return -1;
-      idx >>= 5;
+      idx >>= TF_SHIFT;
       lvl += 1;
     }
     while (lvl > 0) {  // descend: some child of a node <= T is <= T
       lvl -= 1;
-      const int base = node << 5;
-      const unsigned m = __ballot_sync(FULL, p.t_lv[t_off(lvl) + base + lane] <= T);
-      node = base + __ffs(m) - 1;
+      const int base = node << TF_SHIFT;
+      node = base + t_chunk_first(t_off(lvl) + base, 0, T);
     }
     return node;
   }
@@ -405,8 +419,9 @@ struct Eng {
     __syncwarp();
     int idx = b;
     for (int l = 1; l <= cfg.tg.top; ++l) {
-      const int parent = idx >> 5;
-      const int mn = __reduce_min_sync(FULL, p.t_lv[t_off(l - 1) + (parent << 5) + lane]);
+      const int parent = idx >> TF_SHIFT;
+      const int4 v = *reinterpret_cast<const int4*>(p.t_lv + t_off(l - 1) + (parent << TF_SHIFT) + 4 * lane);
+      const int mn = __reduce_min_sync(FULL, min(min(v.x, v.y), min(v.z, v.w)));
       const int at = t_off(l) + parent;
       if (p.t_lv[at] == mn) break;
       __syncwarp();

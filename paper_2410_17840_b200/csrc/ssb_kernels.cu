@@ -606,7 +606,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
       return SSB_E_ARG;
     if (I.engine.policy == SSB_POLICY_TRAIL_PLUS &&
         std::min<long long>(I.engine.max_context, (long long)I.engine.pool_blocks * I.engine.block_size) >= (1LL << 20))
-      return SSB_E_ARG;  // remaining-output buckets: 4 tree levels (2^20 buckets) at most
+      return SSB_E_ARG;  // remaining-output buckets: 3 tree levels (2^20 buckets) at most
     Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
     need = std::max(need, I.scratch_offset + L.total * (long long)I.n_servers);
     if (I.n_servers == 1) singles.push_back(i); else { multis.push_back(i); max_servers = std::max(max_servers, I.n_servers); }
