@@ -326,6 +326,7 @@ struct ClusterShared {
   int done;
   int synced;
   int err;
+  long long fin_cnt, fin_in, fin_out;  // completions of every engine (BetaEstimator sums)
 };
 
 constexpr int CLUSTER_MAX_WARPS = 8;
@@ -345,8 +346,11 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   long long* v_if = smem_ll + 2 * n;   // .in_flight
   long long* rps = smem_ll + 3 * n;    // Σ prompt routed to s
   int* cnt = (int*)(smem_ll + 4 * n);  // arrivals routed to s
+  // lower bound of each engine's next boundary time: an advance phase skips every engine
+  // whose bound is >= its time limit (it would process nothing)
+  double* s_nb = (double*)(smem_ll + 5 * ((n + 1) & ~1));
   // per-server shared running tables when n servers fit (else global tables)
-  int* sm_tabs = (int*)(smem_ll + 5 * ((n + 1) & ~1));
+  int* sm_tabs = (int*)(smem_ll + 6 * ((n + 1) & ~1));
   const bool tabs_in_smem = smem_tabs != 0;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
   const Cfg cfg = make_cfg(I);
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
     v_if[s] = 0;
     rps[s] = 0;
     cnt[s] = 0;
+    s_nb[s] = __longlong_as_double(0x7ff0000000000000LL);  // idle, nothing routed
   }
   {
     Eng E;
@@ -378,11 +383,14 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
     S.k = 0; S.done = 0; S.synced = 1; S.err = 0;
     S.last_poll = 0.0;
     S.beta = I.beta_prior;
+    S.fin_cnt = S.fin_in = S.fin_out = 0;
   }
   __syncthreads();
 
   const bool uses_view = I.balancer == SSB_BAL_P2C || I.balancer == SSB_BAL_SAL;
   const bool est_beta = I.balancer == SSB_BAL_SAL && isnan(I.beta_fixed);
+  const bool cap_pow2 = cfg.cap > 0 && (cfg.cap & (cfg.cap - 1)) == 0;
+  const double inv_cap = cap_pow2 ? __ddiv_rn(1.0, (double)cfg.cap) : 0.0;
   Pcg rng;
   rng.shi = I.pcg_state_hi; rng.slo = I.pcg_state_lo; rng.ihi = I.pcg_inc_hi; rng.ilo = I.pcg_inc_lo;
   rng.has = 0; rng.buf = 0;
@@ -439,7 +447,10 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
           for (int q = lane; q < n; q += 32) {
             // sal_load (balancers.py:103-112)
             double mem = __dmul_rn(beta, (double)((long long)pr - v_f[q]));
-            double que = __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
+            // (queued + prompt) / cap: exact integers (< 2^53); for a power-of-two cap the
+            // correctly rounded quotient is the exact product with 2^-k
+            double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
+                                  : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
             double load = que > mem ? que : mem;
             if (bi == 0x7fffffff || load < best) { best = load; bi = q; }
           }
@@ -464,6 +475,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
           cnt[s] += 1;
           rps[s] += pr;
           rec_srv[k] = s;
+          if (t < s_nb[s]) s_nb[s] = t;  // its boundary is max(t, clock) >= t
         }
         __syncwarp();
         k++;
@@ -479,30 +491,36 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
     __syncthreads();
     // ---------------- advance phase: every replica to its boundaries < t_lim ----------------
     const double t_lim = S.t_lim;
+    long long dc = 0, di = 0, dout = 0;  // this warp's completions (beta sums)
     for (int s = warp; s < n; s += nwarps) {
+      if (!(s_nb[s] < t_lim)) continue;  // no boundary before t_lim: advance would do nothing
       Eng E;
       bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap,
                   tabs_in_smem ? sm_tabs + s * SM_COLS * RS : nullptr);
       Srv* sp = (Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
       E.st = *sp;
+      const long long c0 = E.st.fin_cnt, i0 = E.st.fin_in, o0 = E.st.fin_out;
       E.advance(t_lim, cnt[s]);
+      dc += E.st.fin_cnt - c0; di += E.st.fin_in - i0; dout += E.st.fin_out - o0;
+      const double na = E.next_arrival(cnt[s]);
+      const double nb = E.has_work() ? E.st.clock : (na > E.st.clock ? na : E.st.clock);
       __syncwarp();
       if (lane == 0) {
         *sp = E.st;
+        s_nb[s] = nb;
         if (E.st.status) atomicExch(&S.err, E.st.status);
       }
+    }
+    if (lane == 0 && dc) {
+      atomicAdd((unsigned long long*)&S.fin_cnt, (unsigned long long)dc);
+      atomicAdd((unsigned long long*)&S.fin_in, (unsigned long long)di);
+      atomicAdd((unsigned long long*)&S.fin_out, (unsigned long long)dout);
     }
     __syncthreads();
     // ---------------- sync point: fold beta (on_finish, cluster.py:153-154) ----------------
     if (threadIdx.x == 0) {
-      if (est_beta) {
-        long long c = 0, si = 0, so = 0;
-        for (int s = 0; s < n; ++s) {
-          const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
-          c += sv->fin_cnt; si += sv->fin_in; so += sv->fin_out;
-        }
-        S.beta = c == 0 ? I.beta_prior : __ddiv_rn((double)(si + so), (double)so);  // balancers.py:96-100
-      }
+      if (est_beta)  // balancers.py:96-100 over every engine's completions so far
+        S.beta = S.fin_cnt == 0 ? I.beta_prior : __ddiv_rn((double)(S.fin_in + S.fin_out), (double)S.fin_out);
       S.synced = 1;
       if (S.k >= N || S.err) S.done = 1;
     }
@@ -666,7 +684,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   const int* d_hdr = (const int*)scratch;
   if (!multis.empty()) {
     const int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
-    size_t smc = sizeof(long long) * 5 * ((max_servers + 1) & ~1);
+    size_t smc = sizeof(long long) * 6 * ((max_servers + 1) & ~1);
     if (max_servers <= CLUSTER_SMEM_SERVERS) smc += sizeof(int) * SM_COLS * RS * max_servers;
     if (smc > 48 * 1024) cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
     k_cluster<<<(unsigned)multis.size(), 32 * nw, smc, stream>>>(d_inst, d_hdr + off_multi, trace, records, d_stats,
