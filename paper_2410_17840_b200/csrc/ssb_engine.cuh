@@ -78,6 +78,7 @@ __host__ __device__ inline TrailGeom trail_geom(int max_ctx, int pool, int bs) {
 
 struct Cfg {
   int policy, max_output, bs, bs_shift, pool, cap, max_running, max_ctx;
+  unsigned long long bmul;  // ceil(2^32 / bs): blocks() as one multiply-shift, exact (see blocks)
   int n_servers, Wc, Rc;
   double alpha, c, mem_base, mem_kv, compute, overhead, qps;
   TrailGeom tg;
@@ -174,9 +175,6 @@ __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool
   return warp_argmax_u64(~key, has);
 }
 
-// ceil(t / bs) for block sizes that are not a power of two (kept out of line:
-// the integer division would otherwise be inlined at every call site)
-__device__ __noinline__ int div_up_slow(int t, int bs) { return (t + bs - 1) / bs; }
 
 // FNV-1a over the 64-bit words (code, request id, time bits) of one event
 __device__ __noinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
@@ -302,7 +300,13 @@ struct Eng {
   }
 
   __device__ __forceinline__ int blocks(int tokens) const {  // kvmem.py:15-21
-    return cfg.bs_shift >= 0 ? (tokens + cfg.bs - 1) >> cfg.bs_shift : div_up_slow(tokens, cfg.bs);
+    // floor(n / bs) for n = tokens + bs - 1 as (n * ceil(2^32/bs)) >> 32: with
+    // ceil(2^32/bs) = (2^32 + e)/bs, 0 <= e < bs, the error term n*e/(bs*2^32) stays below
+    // 1/bs (so below 1 - frac(n/bs)) whenever n < 2^32/bs, which ssb_simulate checks for
+    // every token count a request can reach (prompt + output <= max_context). Branch-free:
+    // one code path for every block size (a smaller hot loop than a pow2/divide branch).
+    const unsigned n = (unsigned)(tokens + cfg.bs - 1);
+    return (int)(((unsigned long long)n * cfg.bmul) >> 32);
   }
   __device__ __forceinline__ int phys(int k) const {  // ring slot of logical position k
     int x = st.whead + k;
@@ -1336,6 +1340,54 @@ struct Eng {
     return true;
   }
 
+  // ---- steady-state run: many decode iterations in one tight loop ----
+  // Called right after a fast_decode iteration when nothing can change the schedule:
+  // every running request decoding and cached in registers (regs_ok), select known to
+  // dispatch nothing (nodisp: stays true while only free blocks shrink, see `nodisp`).
+  // Each further iteration is then fully determined by the previous one: one token per
+  // request, grows at block boundaries, clock += iteration_latency(rsum, R) with rsum
+  // += R. It runs while (a) no request would finish (stop one before the first finish:
+  // fast_decode handles that iteration's events), (b) the grows fit the free pool (else
+  // the ordered eviction path must run), (c) the loop-top conditions of advance() hold:
+  // clock < t_lim and no arrival is due (clock < next_t). No events are emitted in
+  // these iterations, so the decision digest is unaffected. Exact: the same binary64
+  // operations in the same order as fast_decode (rsum as an exact double < 2^53).
+  __device__ void fast_forward(double lim) {
+    const int R = st.R;
+    const bool v0 = lane < R, v1 = lane + 32 < R;
+    const int left = min(v0 ? c_out0 - c_g0 : 0x7fffffff, v1 ? c_out1 - c_g1 : 0x7fffffff);
+    const int kmax = (int)__reduce_min_sync(FULL, (unsigned)left) - 1;  // iterations before a finish
+    if (kmax <= 0 || !(st.clock < lim)) return;
+    const int bsm = cfg.bs - 1;
+    const int t0 = c_pr0 + c_g0, t1 = c_pr1 + c_g1;  // KV tokens before the next iteration
+    const double comp = __dmul_rn(cfg.compute, (double)R);
+    const double Rd = (double)R;
+    double clock = st.clock, rs = (double)rsum;
+    int free = st.free_blocks, k = 0;
+    while (k < kmax) {
+      const int need = __popc(__ballot_sync(FULL, v0 && ((t0 + k) & bsm) == 0)) +
+                       __popc(__ballot_sync(FULL, v1 && ((t1 + k) & bsm) == 0));
+      if (need > free) break;
+      const double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, rs));
+      clock = __dadd_rn(clock, __dadd_rn(cfg.overhead, comp > mem ? comp : mem));
+      rs = __dadd_rn(rs, Rd);
+      free -= need;
+      k += 1;
+      if (!(clock < lim)) break;
+    }
+    if (k == 0) return;
+    st.clock = clock;
+    st.free_blocks = free;
+    c_g0 += v0 ? k : 0;
+    c_g1 += v1 ? k : 0;
+    regs_dirty = true;
+    const long long rk = (long long)R * k;
+    rsum += rk;
+    st.rsteps += rk;
+    st.btokens += rk;
+    st.iterations += k;
+  }
+
   // finishes inside a steady-state iteration (_finish, engine.py:360-366)
   __device__ void finish_fast(bool f0, bool f1, unsigned m0, unsigned m1) {
     nodisp = false;
@@ -1457,6 +1509,8 @@ struct Eng {
         next_t = next_arrival(n_avail);
       }
       step();
+      if (regs_ok && nodisp && st.status == SSB_OK && cfg.bs_shift >= 0)
+        fast_forward(next_t < t_lim ? next_t : t_lim);
     }
     drop_regs();  // the table in memory is authoritative between calls
 #ifdef SSB_PHASE_TIMING

@@ -95,6 +95,7 @@ __device__ inline Cfg make_cfg(const ssb_instance& I) {
   c.max_output = e.max_output;
   c.bs = e.block_size;
   c.bs_shift = (e.block_size & (e.block_size - 1)) == 0 ? __ffs(e.block_size) - 1 : -1;
+  c.bmul = (0x100000000ULL + (unsigned long long)e.block_size - 1ULL) / (unsigned long long)e.block_size;
   c.pool = e.pool_blocks;
   c.cap = e.max_tokens_per_batch;
   c.max_running = e.max_running;
@@ -622,6 +623,9 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const ssb_instance& I = h_inst[i];
     if (I.n_servers < 1 || I.n_requests < 0 || I.n_requests > 0x7fffffffLL || I.wait_cap < 1 || I.run_cap < 1)
       return SSB_E_ARG;
+    if (I.engine.block_size < 1 ||
+        ((long long)I.engine.max_context + I.engine.block_size) * I.engine.block_size >= (1LL << 32))
+      return SSB_E_ARG;  // blocks(): multiply-shift division exact for token counts < 2^32 / block_size
     if (I.engine.policy == SSB_POLICY_TRAIL_PLUS &&
         std::min<long long>(I.engine.max_context, (long long)I.engine.pool_blocks * I.engine.block_size) >= (1LL << 20))
       return SSB_E_ARG;  // remaining-output buckets: 3 tree levels (2^20 buckets) at most
