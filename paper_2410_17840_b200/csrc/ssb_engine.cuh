@@ -650,6 +650,9 @@ struct Eng {
       if ((long long)nd >= slots || budget <= 0 || free <= 0) break;  // need >= 1 always
       bool h1 = false, h2 = false;
       LKey b1{0.0, 0.0, 0x7fffffff, -1}, b2{0.0, 0.0, 0x7fffffff, -1};
+      double emin = 1e300;  // (first scan) certification bounds, see below
+      int pmax = 0;
+      const double qld = (double)ql;
       for (int k0 = 0; k0 < st.W; k0 += 64) {  // two independent elements per lane per trip
         LKey x[2];
         bool hx[2];
@@ -663,8 +666,12 @@ struct Eng {
             x[u].enq = p.w_enq[pos];
             x[u].k = k;
             const int pend = p.w_pend[pos];
-            // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending
-            x[u].sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, x[u].enq)), (double)(ql * (long long)pend));
+            emin = fmin(emin, x[u].enq);
+            pmax = max(pmax, pend);
+            // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending; the
+            // int product is < 2^53 (queue_len < 2^31, pending <= max_context), so the
+            // binary64 product of the two exact operands is exact, as Python's int is
+            x[u].sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, x[u].enq)), __dmul_rn(qld, (double)pend));
           }
         }
 #pragma unroll
@@ -685,18 +692,10 @@ struct Eng {
       if (first_scan) {
         first_scan = false;
         // certify the winner for later steps: exact gap to any other candidate >= delta
-        double emin = 1e300;
-        long long pmax = 0;
-        for (int k = lane; k < st.W; k += 32) {
-          const int pos = phys(k);
-          emin = fmin(emin, p.w_enq[pos]);
-          pmax = max(pmax, (long long)p.w_pend[pos]);
-        }
+        // (emin / pmax over the whole waiting set, gathered by the scan above)
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          emin = fmin(emin, __shfl_xor_sync(FULL, emin, o));
-          pmax = max(pmax, __shfl_xor_sync(FULL, pmax, o));
-        }
+        for (int o = 16; o; o >>= 1) emin = fmin(emin, __shfl_xor_sync(FULL, emin, o));
+        pmax = __reduce_max_sync(FULL, (unsigned)pmax);
         const double E0 = (3.0 * cfg.alpha * (st.clock - emin) + (double)(ql * pmax)) * 1.1102230246251565e-16 * 1.0001;
         const double sc2 = w2 ? __shfl_sync(FULL, rc.sc, __ffs(w2) - 1) : -1e300;
         lc_delta = w2 ? (top.sc - sc2) - 2.0 * E0 : 1e300;  // a single candidate leads by infinity

@@ -626,6 +626,8 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     if (I.engine.block_size < 1 ||
         ((long long)I.engine.max_context + I.engine.block_size) * I.engine.block_size >= (1LL << 32))
       return SSB_E_ARG;  // blocks(): multiply-shift division exact for token counts < 2^32 / block_size
+    if (I.engine.policy == SSB_POLICY_LARRY && I.engine.max_context >= (1 << 22))
+      return SSB_E_ARG;  // larry_score: queue_len * pending < 2^31 * 2^22 is exact in binary64
     if (I.engine.policy == SSB_POLICY_TRAIL_PLUS &&
         std::min<long long>(I.engine.max_context, (long long)I.engine.pool_blocks * I.engine.block_size) >= (1LL << 20))
       return SSB_E_ARG;  // remaining-output buckets: 3 tree levels (2^20 buckets) at most
