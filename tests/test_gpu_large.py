@@ -1,0 +1,83 @@
+"""Larger BASELINE-shaped runs on the CUDA path vs the oracle (bit-exact), sized so
+each finishes in seconds: C5 (64-replica SAL and RR clusters) on its first 600 s
+(~134k requests per instance), C3 (tight pool, long tails, recompute-on-resume) on
+its first 20,000 s, and the full C4 sweep of one seed (256 instances). Plus
+size-independent properties at those sizes: every request finished exactly once,
+event-time ordering of the records, preemption counts consistent with the counters,
+and run-to-run determinism of the decision digests."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "parks", "finished",
+        "peak_batch_tokens", "digest", "status")
+
+
+def _run(jobs):
+    import torch
+
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200 import simulate
+
+    batch = I.make_batch(jobs)
+    rec, st = simulate.run_batch(batch, check=True)
+    torch.cuda.synchronize()
+    return batch, rec, st
+
+
+def _check_vs_oracle(batch, rec, st):
+    orec, ost = O.run_batch(batch, threads=8)
+    for k in KEYS:
+        assert np.array_equal(st[k], ost[k]), k
+    for col in ("first_token", "finish", "first_dispatch"):
+        assert np.array_equal(getattr(rec, col).view(np.int64), getattr(orec, col).view(np.int64)), col
+    for col in ("preempt_count", "server"):
+        assert np.array_equal(getattr(rec, col), getattr(orec, col)), col
+
+
+def _properties(batch, rec, st):
+    assert (st["status"] == 0).all()
+    assert int(st["finished"].sum()) == batch.n_records
+    for inst in batch.instances:
+        o, t, n, f = int(inst["record_offset"]), int(inst["trace_offset"]), int(inst["n_requests"]), float(inst["qps_factor"])
+        arr = batch.trace.arrival[t:t + n] / f
+        fd, ft, fin = rec.first_dispatch[o:o + n], rec.first_token[o:o + n], rec.finish[o:o + n]
+        assert np.isfinite(fin).all()
+        assert (arr <= fd).all() and (fd <= ft).all() and (ft <= fin).all()
+        assert ((rec.server[o:o + n] >= 0) & (rec.server[o:o + n] < int(inst["n_servers"]))).all()
+    # a preempted request is counted once per preemption/park (engine.py:368-379)
+    assert int(rec.preempt_count.sum()) == int(st["preempts"].sum() + st["parks"].sum())
+    # each dispatch is a first dispatch or a re-dispatch after a preemption
+    assert int(st["dispatches"].sum()) == batch.n_records + int(rec.preempt_count.sum())
+
+
+def test_c5_prefix_64_replicas_matches_oracle():
+    from paper_2410_17840_b200 import configs as C
+
+    batch, rec, st = _run(C.c5_jobs(600.0))
+    _properties(batch, rec, st)
+    _check_vs_oracle(batch, rec, st)
+
+
+def test_c3_prefix_preemption_regime_matches_oracle():
+    from paper_2410_17840_b200 import configs as C
+
+    batch, rec, st = _run(C.c3_jobs(20000.0))
+    _properties(batch, rec, st)
+    assert int(st["preempts"].sum()) > 1000  # the regime this config exists for
+    _check_vs_oracle(batch, rec, st)
+
+
+def test_c4_seed_sweep_matches_oracle_and_is_deterministic():
+    from paper_2410_17840_b200 import configs as C
+
+    jobs = C.c4_jobs(seeds=[5])
+    batch, rec, st = _run(jobs)
+    _properties(batch, rec, st)
+    _check_vs_oracle(batch, rec, st)
+    _, _, st2 = _run(jobs)
+    assert np.array_equal(st["digest"], st2["digest"])
