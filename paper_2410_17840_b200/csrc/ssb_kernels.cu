@@ -15,9 +15,12 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "ssb_engine.cuh"
 
 using namespace ssb;
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -317,8 +320,13 @@ struct Pcg {
 };
 
 // ------------------------------------------------------------------------
-// multi-server instances: one CTA each
+// multi-server instances: one thread-block cluster each (1..8 CTAs x 8 warps)
 // ------------------------------------------------------------------------
+// The routing state (S, the BalancerView columns, per-server routed counts, next-boundary
+// bounds) lives in the shared memory of the cluster's rank-0 CTA; the other CTAs read and
+// write it through distributed shared memory. Warp w of CTA r advances servers
+// r*8+w, r*8+w + 8*G, ... so a 64-replica instance (C5) gets one warp per replica on
+// 8 SMs instead of 8 replicas per warp on one; cluster barriers separate the phases.
 struct ClusterShared {
   double t_lim;
   double last_poll;
@@ -327,66 +335,81 @@ struct ClusterShared {
   int done;
   int synced;
   int err;
+  int epochs, polls;  // routing phases / view refreshes (cost diagnostics)
   long long fin_cnt, fin_in, fin_out;  // completions of every engine (BetaEstimator sums)
 };
 
 constexpr int CLUSTER_MAX_WARPS = 8;
-constexpr int CLUSTER_SMEM_SERVERS = 12;  // 12 x 15 KiB shared running tables
+constexpr int CLUSTER_MAX_CTAS = 8;       // portable cluster size
+constexpr int CLUSTER_SMEM_SERVERS = 12;  // shared running tables per CTA (12 x 16 KiB)
 
 __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr,
                           ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch,
                           ssb_event* events, long long ev_cap, int64_t* ev_count, int smem_tabs) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
   extern __shared__ long long smem_ll[];
-  __shared__ ClusterShared S;
-  const int idx = order[blockIdx.x];
+  __shared__ ClusterShared S_own;
+  const int idx = order[blockIdx.x / G];
   const ssb_instance I = inst[idx];
   const int n = I.n_servers;
   const long long N = I.n_requests;
-  long long* v_q = smem_ll;            // BalancerView.stats[s].queued_tokens
-  long long* v_f = smem_ll + n;        // .free_mem_tokens
-  long long* v_if = smem_ll + 2 * n;   // .in_flight
-  long long* rps = smem_ll + 3 * n;    // Σ prompt routed to s
-  int* cnt = (int*)(smem_ll + 4 * n);  // arrivals routed to s
+  // rank 0 owns the routing state; everyone addresses it through one generic pointer
+  long long* R0 = rank == 0 ? smem_ll : cl.map_shared_rank(smem_ll, 0);
+  ClusterShared& S = *(rank == 0 ? &S_own : cl.map_shared_rank(&S_own, 0));
+  long long* v_q = R0;               // BalancerView.stats[s].queued_tokens
+  long long* v_f = R0 + n;           // .free_mem_tokens
+  long long* v_if = R0 + 2 * n;      // .in_flight
+  long long* rps = R0 + 3 * n;       // Σ prompt routed to s
+  int* cnt = (int*)(R0 + 4 * n);     // arrivals routed to s
   // lower bound of each engine's next boundary time: an advance phase skips every engine
   // whose bound is >= its time limit (it would process nothing)
-  double* s_nb = (double*)(smem_ll + 5 * ((n + 1) & ~1));
-  // per-server shared running tables when n servers fit (else global tables)
+  double* s_nb = (double*)(R0 + 5 * ((n + 1) & ~1));
+  // this CTA's shared running tables (its own servers), when they fit
   int* sm_tabs = (int*)(smem_ll + 6 * ((n + 1) & ~1));
   const bool tabs_in_smem = smem_tabs != 0;
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+  const int gw = rank * nwarps + warp, GW = G * nwarps;  // cluster-wide warp index / count
+  // cluster barrier (also orders the DSMEM and global accesses around it); a one-CTA
+  // cluster (<= 8 replicas) uses the cheaper CTA barrier
+  auto csync = [&]() { if (G == 1) __syncthreads(); else cl.sync(); };
+  auto tab_of = [&](int s) { return tabs_in_smem ? sm_tabs + ((s / GW) * nwarps + warp) * SM_COLS * RS : nullptr; };
   const Cfg cfg = make_cfg(I);
   const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
 
   // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
-  for (int s = warp; s < n; s += nwarps) {
+  for (int s = gw; s < n; s += GW) {
     Eng E;
-    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tabs_in_smem ? sm_tabs + s * SM_COLS * RS : nullptr);
+    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab_of(s));
     init_srv(E.st, cfg);
     if (cfg.policy == SSB_POLICY_TRAIL_PLUS) E.trail_init();
     fill_events(E, lane, 32);
     if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
   }
-  for (int s = threadIdx.x; s < n; s += blockDim.x) {
-    v_q[s] = 0;
-    v_f[s] = (long long)cfg.pool * cfg.bs;
-    v_if[s] = 0;
-    rps[s] = 0;
-    cnt[s] = 0;
-    s_nb[s] = __longlong_as_double(0x7ff0000000000000LL);  // idle, nothing routed
+  if (rank == 0) {
+    for (int s = threadIdx.x; s < n; s += blockDim.x) {
+      v_q[s] = 0;
+      v_f[s] = (long long)cfg.pool * cfg.bs;
+      v_if[s] = 0;
+      rps[s] = 0;
+      cnt[s] = 0;
+      s_nb[s] = __longlong_as_double(0x7ff0000000000000LL);  // idle, nothing routed
+    }
+    if (threadIdx.x == 0) {
+      S.k = 0; S.done = 0; S.synced = 1; S.err = 0; S.epochs = 0; S.polls = 0;
+      S.last_poll = 0.0;
+      S.beta = I.beta_prior;
+      S.fin_cnt = S.fin_in = S.fin_out = 0;
+    }
   }
   {
     Eng E;
     bind_engine(E, I, cfg, scratch, 0, L, tr, rec, evb, ev_cap);
-    clear_records(E, N, threadIdx.x, blockDim.x);
+    clear_records(E, N, rank * blockDim.x + threadIdx.x, G * blockDim.x);
   }
-  if (threadIdx.x == 0) {
-    S.k = 0; S.done = 0; S.synced = 1; S.err = 0;
-    S.last_poll = 0.0;
-    S.beta = I.beta_prior;
-    S.fin_cnt = S.fin_in = S.fin_out = 0;
-  }
-  __syncthreads();
+  csync();
 
   const bool uses_view = I.balancer == SSB_BAL_P2C || I.balancer == SSB_BAL_SAL;
   const bool est_beta = I.balancer == SSB_BAL_SAL && isnan(I.beta_fixed);
@@ -402,8 +425,8 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   const double poll = I.poll_interval_s;
 
   while (true) {
-    // ---------------- routing phase (warp 0) ----------------
-    if (warp == 0) {
+    // ---------------- routing phase (warp 0 of rank 0) ----------------
+    if (rank == 0 && warp == 0) {
       int k = S.k;
       int synced = S.synced;
       double last_poll = S.last_poll;
@@ -422,6 +445,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
           }
           __syncwarp();
           last_poll = t;
+          if (lane == 0) S.polls += 1;
         }
         int s = 0;
         if (I.balancer == SSB_BAL_RR) {  // balancers.py:139-142
@@ -438,10 +462,29 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
           }
         } else {  // SAL (:204-212)
           if (est_beta && !synced) {
-            // the argmin is beta-independent iff every server has free_mem >= prompt
-            bool dep = false;
-            for (int q = lane; q < n; q += 32) dep |= v_f[q] < pr;
-            if (__any_sync(FULL, dep)) break;
+            // beta (balancers.py:96-100) moves with completions the routing warp has not
+            // seen; the route needs it only if the argmin can depend on it. A server with
+            // free_mem >= prompt has load == its queue term Q (beta*(prompt-free) <= 0 < Q);
+            // one with free_mem < prompt has load >= Q for every beta. So if the best
+            // unconstrained (Q, index) beats every constrained server's (Q, index), it wins
+            // for every beta and no barrier is needed.
+            double bu = 0.0, bc = 0.0;
+            int iu = 0x7fffffff, ic = 0x7fffffff;
+            for (int q = lane; q < n; q += 32) {
+              const double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
+                                          : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
+              if (v_f[q] < pr) { if (ic == 0x7fffffff || que < bc) { bc = que; ic = q; } }
+              else if (iu == 0x7fffffff || que < bu) { bu = que; iu = q; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              const double ou = __shfl_xor_sync(FULL, bu, o), oc = __shfl_xor_sync(FULL, bc, o);
+              const int jou = __shfl_xor_sync(FULL, iu, o), joc = __shfl_xor_sync(FULL, ic, o);
+              if (jou != 0x7fffffff && (iu == 0x7fffffff || ou < bu || (ou == bu && jou < iu))) { bu = ou; iu = jou; }
+              if (joc != 0x7fffffff && (ic == 0x7fffffff || oc < bc || (oc == bc && joc < ic))) { bc = oc; ic = joc; }
+            }
+            const bool indep = ic == 0x7fffffff || (iu != 0x7fffffff && (bu < bc || (bu == bc && iu < ic)));
+            if (!indep) break;
           }
           double best = 0.0;
           int bi = 0x7fffffff;
@@ -489,15 +532,14 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
         S.t_lim = k < N ? __ddiv_rn(arr[k], I.qps_factor) : __longlong_as_double(0x7ff0000000000000LL);
       }
     }
-    __syncthreads();
+    csync();
     // ---------------- advance phase: every replica to its boundaries < t_lim ----------------
     const double t_lim = S.t_lim;
     long long dc = 0, di = 0, dout = 0;  // this warp's completions (beta sums)
-    for (int s = warp; s < n; s += nwarps) {
+    for (int s = gw; s < n; s += GW) {
       if (!(s_nb[s] < t_lim)) continue;  // no boundary before t_lim: advance would do nothing
       Eng E;
-      bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap,
-                  tabs_in_smem ? sm_tabs + s * SM_COLS * RS : nullptr);
+      bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab_of(s));
       Srv* sp = (Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
       E.st = *sp;
       const long long c0 = E.st.fin_cnt, i0 = E.st.fin_in, o0 = E.st.fin_out;
@@ -517,20 +559,22 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
       atomicAdd((unsigned long long*)&S.fin_in, (unsigned long long)di);
       atomicAdd((unsigned long long*)&S.fin_out, (unsigned long long)dout);
     }
-    __syncthreads();
+    csync();
     // ---------------- sync point: fold beta (on_finish, cluster.py:153-154) ----------------
-    if (threadIdx.x == 0) {
+    if (rank == 0 && threadIdx.x == 0) {
       if (est_beta)  // balancers.py:96-100 over every engine's completions so far
         S.beta = S.fin_cnt == 0 ? I.beta_prior : __ddiv_rn((double)(S.fin_in + S.fin_out), (double)S.fin_out);
       S.synced = 1;
+      S.epochs += 1;
       if (S.k >= N || S.err) S.done = 1;
     }
-    __syncthreads();
+    csync();
     if (S.done) break;
   }
+  csync();  // every CTA has read S.done: rank 0's shared memory may go away after this
 
   // ---------------- per-instance stats ----------------
-  if (threadIdx.x == 0) {
+  if (rank == 0 && threadIdx.x == 0) {
     ssb_stats out;
     memset(&out, 0, sizeof(out));
     unsigned long long h = FNV_OFF;
@@ -553,6 +597,10 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
     if (!status && out.finished != N) status = SSB_E_INVARIANT;  // cluster.py:159-161
     out.digest = h;
     out.status = status;
+#ifdef SSB_EPOCH_PROBE
+    out._pad = S.epochs;
+    out.device_cycles = S.polls;
+#endif
     stats[idx] = out;
     if (ev_count) ev_count[idx] = evn;
   }
@@ -689,13 +737,29 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     return SSB_E_CUDA;
   const int* d_hdr = (const int*)scratch;
   if (!multis.empty()) {
+    // one cluster of G CTAs x nw warps per instance: enough warps for one replica each (<= 64)
     const int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
+    const int G = std::min(CLUSTER_MAX_CTAS, (max_servers + nw - 1) / nw);
+    const int per_warp = (max_servers + G * nw - 1) / (G * nw);  // replicas per warp
+    const int tabs = per_warp * nw <= CLUSTER_SMEM_SERVERS ? 1 : 0;
     size_t smc = sizeof(long long) * 6 * ((max_servers + 1) & ~1);
-    if (max_servers <= CLUSTER_SMEM_SERVERS) smc += sizeof(int) * SM_COLS * RS * max_servers;
+    if (tabs) smc += sizeof(int) * SM_COLS * RS * per_warp * nw;
     if (smc > 48 * 1024) cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-    k_cluster<<<(unsigned)multis.size(), 32 * nw, smc, stream>>>(d_inst, d_hdr + off_multi, trace, records, d_stats,
-                                                               scratch, d_events, event_cap, d_event_count,
-                                                               max_servers <= CLUSTER_SMEM_SERVERS ? 1 : 0);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(multis.size() * G));
+    lc.blockDim = dim3(32 * nw);
+    lc.dynamicSmemBytes = smc;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, k_cluster, (const ssb_instance*)d_inst, (const int*)(d_hdr + off_multi), trace, records,
+                           d_stats, scratch, d_events, (long long)event_cap, (int64_t*)d_event_count, tabs) != cudaSuccess)
+      return SSB_E_CUDA;
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   if (!singles.empty()) {
