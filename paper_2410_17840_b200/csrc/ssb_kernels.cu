@@ -248,27 +248,41 @@ __device__ __forceinline__ unsigned sm_id() {
 // longest estimated cost first, and steals from the other queues once its own is empty.
 // Keeping one policy per SM keeps the policy-specific code of each SM's warps the same.
 struct EngineQueues {
-  int n[4];      // instances per policy
-  int off[4];    // offset of each policy's order list in order[]
+  int n[5];      // instances per queue: 4 policies + (queue 4) the longest trail_plus instances
+  int off[5];    // offset of each queue's order list in order[]
 };
+constexpr int Q_HEAVY = 4;
 __global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA, 1)
 k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, EngineQueues qs,
-          int* __restrict__ queue, const unsigned char* __restrict__ sm_policy, int n_sm_policy, ssb_trace tr,
-          ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch, ssb_event* events,
-          long long ev_cap, int64_t* ev_count) {
+          int* __restrict__ queue, const unsigned char* __restrict__ sm_policy, int n_sm_policy,
+          int* __restrict__ sm_slot, ssb_trace tr, ssb_records rec,
+          ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
+          int64_t* ev_count) {
   extern __shared__ int sm_engines[];
+  __shared__ int s_slot;
   int* sm_tab = sm_engines + (threadIdx.x >> 5) * (SM_COLS * RS);  // this warp's running table
   const int lane = lane_id();
   const unsigned smid = sm_id();
-  int pol = smid < (unsigned)n_sm_policy ? sm_policy[smid] : 0;
-  int tried = 0;
-  while (tried < 4) {
+  const int first = smid < (unsigned)n_sm_policy ? sm_policy[smid] : 0;
+  if (first == Q_HEAVY) {  // SMs of the longest instances run one CTA (see ssb_simulate)
+    if (threadIdx.x == 0) s_slot = atomicAdd(sm_slot + smid, 1);
+    __syncthreads();
+    if (s_slot > 0) return;
+  }
+  // queue order: own queue, then the others (the heavy queue last unless it is ours)
+  int seq[5], nseq = 0;
+  seq[nseq++] = first;
+  if (first == Q_HEAVY) seq[nseq++] = SSB_POLICY_TRAIL_PLUS;
+  for (int k = 1; k < 4; ++k) seq[nseq++] = ((first == Q_HEAVY ? SSB_POLICY_TRAIL_PLUS : first) + k) & 3;
+  if (first != Q_HEAVY) seq[nseq++] = Q_HEAVY;
+  int k = 0;
+  while (k < nseq) {
+    const int pol = seq[k];
     int q = 0;
     if (lane == 0) q = atomicAdd(queue + pol, 1);
     q = __shfl_sync(FULL, q, 0);
     if (q >= qs.n[pol]) {  // this queue is drained: steal from the next one
-      pol = (pol + 1) & 3;
-      tried += 1;
+      k += 1;
       continue;
     }
     run_instance(inst, order[qs.off[pol] + q], tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab);
@@ -611,7 +625,10 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
 // ==========================================================================
 // C ABI
 // ==========================================================================
-static long long header_bytes(int n_inst) { return align_up(64 + 8LL * n_inst, 256); }
+// scheduling header of ssb_simulate: queue counters, per-SM policy table and CTA slot
+// counters (sized for up to MAX_SMS SMs), instance order lists
+constexpr int MAX_SMS = 1024;
+static long long header_bytes(int n_inst) { return align_up(4LL * (16 + (MAX_SMS + 3) / 4 + 4 + MAX_SMS) + 8LL * n_inst, 256); }
 
 extern "C" int32_t ssb_abi_version(void) { return SSB_ABI_VERSION; }
 
@@ -699,37 +716,61 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // header (ints): [queue counters x4, pad x12][sm policy table (bytes)][singles by policy][multis]
-  const int smtab_ints = (sms + 3) / 4 + 4;
-  std::vector<int> hdr(16 + smtab_ints + n_inst, 0);
+  const int sms_tab = std::min(sms, MAX_SMS);
+  // header (ints): [queue counters x4, pad x12][sm policy table (bytes)][per-SM CTA slot
+  // counters][singles by policy][multis]
+  const int smtab_ints = (MAX_SMS + 3) / 4 + 4;
+  const int hdr0 = 16 + smtab_ints + MAX_SMS;
+  std::vector<int> hdr(hdr0 + n_inst, 0);
+  // The longest trail_plus instances (the critical path of a sweep) get SMs of their own
+  // with one CTA (4 warps): trail_plus is instruction-fetch bound, so 4 warps keep the
+  // SM's throughput while each instance runs faster than among 8 (profiles/).
+  int heavy_sms = 0;
+  if (const char* e = getenv("SSB_HEAVY_SMS")) heavy_sms = std::max(0, atoi(e));  // experiments
+  heavy_sms = std::min<int>(heavy_sms, (int)sg[SSB_POLICY_TRAIL_PLUS].size() / ENGINE_WARPS_PER_CTA);
+  heavy_sms = std::min(heavy_sms, sms_tab / 2);
+  const int n_heavy = heavy_sms * ENGINE_WARPS_PER_CTA;
+  std::vector<int> heavy(sg[SSB_POLICY_TRAIL_PLUS].begin(), sg[SSB_POLICY_TRAIL_PLUS].begin() + n_heavy);
+  sg[SSB_POLICY_TRAIL_PLUS].erase(sg[SSB_POLICY_TRAIL_PLUS].begin(), sg[SSB_POLICY_TRAIL_PLUS].begin() + n_heavy);
+  total_work = 0;
+  for (int p = 0; p < 4; ++p) {
+    gwork[p] = 0;
+    for (int i : sg[p]) gwork[p] += (double)std::max(1, h_inst[i].est_cost);
+    total_work += gwork[p];
+  }
+  const int sms_rest = sms_tab - heavy_sms;
   unsigned char* smpol = (unsigned char*)(hdr.data() + 16);
+  for (int k = 0; k < heavy_sms; ++k) smpol[sms_rest + k] = (unsigned char)Q_HEAVY;
   {  // SMs per policy in proportion to estimated work (largest remainder), >= 1 if it has work
     int cnt[4] = {0, 0, 0, 0}, given = 0;
     double rem[4];
     for (int p = 0; p < 4; ++p) {
-      const double want = total_work > 0 ? sms * gwork[p] / total_work : 0.0;
+      const double want = total_work > 0 ? sms_rest * gwork[p] / total_work : 0.0;
       cnt[p] = sg[p].empty() ? 0 : std::max(1, (int)want);
       rem[p] = want - cnt[p];
       given += cnt[p];
     }
-    while (given > sms) {
+    while (given > sms_rest) {
       int pm = 0;
       for (int p = 1; p < 4; ++p) if (cnt[p] > cnt[pm]) pm = p;
       cnt[pm]--; given--;
     }
-    while (given < sms) {
+    while (given < sms_rest) {
       int pm = -1;
       for (int p = 0; p < 4; ++p) if (!sg[p].empty() && (pm < 0 || rem[p] > rem[pm])) pm = p;
       if (pm < 0) break;
       cnt[pm]++; rem[pm] -= 1.0; given++;
     }
     int s0 = 0;
-    for (int p = 0; p < 4; ++p) for (int k = 0; k < cnt[p] && s0 < sms; ++k) smpol[s0++] = (unsigned char)p;
-    for (; s0 < sms; ++s0) smpol[s0] = 0;
+    for (int p = 0; p < 4; ++p) for (int k = 0; k < cnt[p] && s0 < sms_rest; ++k) smpol[s0++] = (unsigned char)p;
+    for (; s0 < sms_rest; ++s0) smpol[s0] = 0;
   }
   EngineQueues qs;
-  int o = 16 + smtab_ints;
-  for (int p = 0; p < 4; ++p) { qs.off[p] = o - (16 + smtab_ints); qs.n[p] = (int)sg[p].size(); for (int i : sg[p]) hdr[o++] = i; }
+  int o = hdr0;
+  for (int p = 0; p < 4; ++p) { qs.off[p] = o - hdr0; qs.n[p] = (int)sg[p].size(); for (int i : sg[p]) hdr[o++] = i; }
+  qs.off[Q_HEAVY] = o - hdr0;
+  qs.n[Q_HEAVY] = (int)heavy.size();
+  for (int i : heavy) hdr[o++] = i;
   const int off_multi = o;
   for (int i : multis) hdr[o++] = i;
   unsigned char* scratch = (unsigned char*)d_scratch;
@@ -770,8 +811,8 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     if (const char* cap = getenv("SSB_CTAS_PER_SM")) occ = std::min(occ, std::max(1, atoi(cap)));  // experiments
     const int grid = sms * std::max(1, occ);
     k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(
-        d_inst, d_hdr + 16 + smtab_ints, qs, (int*)scratch, (const unsigned char*)(d_hdr + 16), sms, trace, records,
-        d_stats, scratch, d_events, event_cap, d_event_count);
+        d_inst, d_hdr + hdr0, qs, (int*)scratch, (const unsigned char*)(d_hdr + 16), sms_tab,
+        (int*)scratch + 16 + smtab_ints, trace, records, d_stats, scratch, d_events, event_cap, d_event_count);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   return SSB_OK;

@@ -44,6 +44,26 @@ def estimate_cost(batch: Batch) -> np.ndarray:
     return np.clip(out // 16, 0, 2**31 - 1)
 
 
+def measured_cost(h_inst: np.ndarray, stats: np.ndarray) -> np.ndarray | None:
+    """Scheduling hint from a finished run: each instance's iteration count times its
+    policy's mean device cycles per iteration (over that policy's instances). Raw
+    per-instance cycles depend on what shared the SM with the instance (up to ~3x for
+    trail_plus), so a schedule built from them oscillates between runs; iterations are
+    exact and the per-policy mean absorbs the contention. None if nothing was measured."""
+    cyc = np.asarray(stats["device_cycles"], dtype=np.float64)
+    it = np.asarray(stats["iterations"], dtype=np.float64)
+    if len(cyc) == 0 or not (cyc > 0).all():
+        return None
+    pol = h_inst["engine"]["policy"]
+    multi = h_inst["n_servers"] > 1
+    cost = cyc.copy()
+    for p in np.unique(pol):
+        m = (pol == p) & ~multi
+        if m.any() and it[m].sum() > 0:
+            cost[m] = it[m] * (cyc[m].sum() / it[m].sum())
+    return np.clip(cost // 1024, 1, 2**31 - 1).astype(h_inst["est_cost"].dtype)
+
+
 @dataclass
 class DeviceBatch:
     """All device buffers of one batch (inputs resident in HBM)."""

@@ -121,12 +121,15 @@ class SweepRunner:
         return (self.p_stats.numpy().view(_abi.STATS).copy(), self.p_summary.numpy().view(_abi.SUMMARY).copy())
 
     def adopt_measured_schedule(self, stats) -> None:
-        """Use each instance's measured device cycles (ssb_stats.device_cycles) as its
-        scheduling hint for later runs of this sweep: per-policy kernel shares of the GPU
-        and longest-first queue order. Work is unchanged; only the placement adapts."""
-        cyc = np.asarray(stats["device_cycles"], dtype=np.int64)
-        if (cyc > 0).all():
-            self.h_inst["est_cost"] = np.clip(cyc // 1024, 1, 2**31 - 1)
+        """Use the measured cost of each instance (simulate.measured_cost: iterations x its
+        policy's mean device cycles per iteration) as its scheduling hint for later runs of
+        this sweep: per-policy SM shares, the SMs reserved for the longest instances, and
+        longest-first queue order. Work is unchanged; only the placement adapts."""
+        from .simulate import measured_cost
+
+        c = measured_cost(self.h_inst, stats)
+        if c is not None:
+            self.h_inst["est_cost"] = c
 
     def fix_overflows(self) -> int:
         """Re-run instances whose shared running table overflowed (then re-summarize)."""

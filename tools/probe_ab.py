@@ -18,8 +18,9 @@ def timed(jobs, reps=3):
     simulate.launch(db)
     torch.cuda.synchronize()
     st = simulate.download(db)[1]
-    if (st["device_cycles"] > 0).all():
-        db.h_inst["est_cost"] = np.clip(st["device_cycles"] // 1024, 1, 2**31 - 1)
+    c = simulate.measured_cost(db.h_inst, st)
+    if c is not None:
+        db.h_inst["est_cost"] = c
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

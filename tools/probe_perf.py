@@ -21,8 +21,9 @@ def gpu_time(batch, reps=3):
     simulate.launch(db)
     torch.cuda.synchronize()
     st0 = simulate.download(db)[1]
-    if (st0["device_cycles"] > 0).all():
-        db.h_inst["est_cost"] = np.clip(st0["device_cycles"] // 1024, 1, 2**31 - 1)
+    c = simulate.measured_cost(db.h_inst, st0)
+    if c is not None:
+        db.h_inst["est_cost"] = c
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
