@@ -524,6 +524,7 @@ struct Eng {
     if (state == ST_DECODE) st.ndec -= 1;
     else st.pf_pend -= (long long)(alloc - pfd);
     if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= wkey_for(pr, out, gen);
+    __syncwarp();  // every lane's reads of entry j (caller) happen before lane 0 rewrites it
     if (lane == 0) {
       p.r_st[j] = ST_GONE;
       rec_pc[rid] += 1;

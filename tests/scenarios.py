@@ -151,7 +151,7 @@ def c3_scenarios(n_inst=100):
     return out
 
 
-def fuzz_engine_scenarios(n=240, seed=90210):
+def fuzz_engine_scenarios(n=240, seed=90210, block_sizes=(1, 4, 8, 16), prefix="fuzz"):
     """Randomised single-engine instances biased toward the hard paths: tight
     pools (grow evictions, recompute), trail_plus with c>0 (policy preempts),
     larry under backlog, max_running caps, small token budgets, ties."""
@@ -160,7 +160,7 @@ def fuzz_engine_scenarios(n=240, seed=90210):
     pols = ["fcfs", "nopreempt", "trail_plus", "larry"]
     for i in range(n):
         pol = pols[i % 4]
-        bs = int(rng.choice([1, 4, 8, 16]))
+        bs = int(rng.choice(list(block_sizes)))
         nreq = int(rng.integers(1, 60))
         burst = rng.random() < 0.4
         if burst:
@@ -182,7 +182,7 @@ def fuzz_engine_scenarios(n=240, seed=90210):
         cost = [float(rng.choice([1e-3, 1e-2])), float(rng.choice([0.0, 1e-6, 8.4e-8])),
                 float(rng.choice([1e-5, 1e-4])), float(rng.choice([0.0, 5e-4]))]
         tr = [(float(a), int(p), int(o)) for a, p, o in zip(arrivals, prompts, outputs)]
-        out.append(scen(f"fuzz_{pol}_{i}", engine(pol, alpha=alpha, c=c, max_output=max_out, pool_blocks=pool,
+        out.append(scen(f"{prefix}_{pol}_{i}", engine(pol, alpha=alpha, c=c, max_output=max_out, pool_blocks=pool,
                                                   block_size=bs, cost=cost, cap=cap, max_running=max_running),
                         rows(tr)))
     return out
@@ -234,7 +234,7 @@ def cluster_unit_scenarios():
     return out
 
 
-def fuzz_cluster_scenarios(n=96, seed=31337):
+def fuzz_cluster_scenarios(n=96, seed=31337, block_sizes=(4, 16), prefix="fuzzcl"):
     """Randomised multi-replica instances: every balancer x policy, tight pools,
     poll intervals from 1 ms to inf, fixed and estimated beta, equal-time bursts."""
     rng = np.random.default_rng(seed)
@@ -250,7 +250,7 @@ def fuzz_cluster_scenarios(n=96, seed=31337):
             arrivals = np.sort(np.round(rng.uniform(0, 1.0, nreq), 1))
         else:
             arrivals = np.sort(rng.exponential(float(rng.choice([0.002, 0.02, 0.2])), nreq).cumsum())
-        bs = int(rng.choice([4, 16]))
+        bs = int(rng.choice(list(block_sizes)))
         prompts = rng.integers(1, int(rng.choice([64, 600, 3000])) + 1, nreq)
         max_out = int(rng.choice([8, 60, 300]))
         outputs = rng.integers(1, max_out + 1, nreq)
@@ -263,7 +263,7 @@ def fuzz_cluster_scenarios(n=96, seed=31337):
         beta_fixed = None if rng.random() < 0.6 else float(rng.choice([1.0, 2.0, 6.5]))
         c = float(rng.choice([0.0, 0.5, 1.0])) if pol == "trail_plus" else 0.0
         tr = [(float(a), int(p), int(o)) for a, p, o in zip(arrivals, prompts, outputs)]
-        out.append(scen(f"fuzzcl_{b}_{pol}_{i}",
+        out.append(scen(f"{prefix}_{b}_{pol}_{i}",
                         engine(pol, c=c, max_output=max_out, pool_blocks=pool, block_size=bs, cost=COST_A100_8B,
                                cap=cap),
                         rows(tr), mode="cluster",
@@ -326,4 +326,8 @@ GROUPS = {
     "cluster_unit": cluster_unit_scenarios,
     "fuzz_cluster": fuzz_cluster_scenarios,
     "configs": config_scenarios,
+    # block sizes that are not powers of two (the device's blocks() is a multiply-shift
+    # division there and the steady-state decode paths are off)
+    "fuzz_odd_blocks": lambda: fuzz_engine_scenarios(80, seed=4242, block_sizes=(3, 5, 10, 12, 24), prefix="odd")
+    + fuzz_cluster_scenarios(24, seed=4243, block_sizes=(3, 10, 24), prefix="oddcl"),
 }
