@@ -171,6 +171,12 @@ __device__ __forceinline__ unsigned warp_argmax_u64(unsigned long long key, bool
   unsigned m2 = __reduce_max_sync(FULL, lo);
   return __ballot_sync(FULL, c1 && lo == m2);
 }
+// warp minimum of a 64-bit key (uniform): two REDUX.MIN on the halves
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long key) {
+  const unsigned hi = __reduce_min_sync(FULL, (unsigned)(key >> 32));
+  const unsigned lo = __reduce_min_sync(FULL, (unsigned)(key >> 32) == hi ? (unsigned)key : 0xffffffffu);
+  return ((unsigned long long)hi << 32) | lo;
+}
 __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool has) {
   return warp_argmax_u64(~key, has);
 }

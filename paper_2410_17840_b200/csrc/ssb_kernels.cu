@@ -437,17 +437,73 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   const int* prm = tr.prompt + I.trace_offset;
   int* rec_srv = rec.server + I.record_offset;
   const double poll = I.poll_interval_s;
+#ifdef SSB_EPOCH_PROBE
+  long long pr_route = 0, pr_sync = 0, pr_adv_own = 0;
+#endif
 
   while (true) {
+#ifdef SSB_EPOCH_PROBE
+    const long long pt0 = clock64();
+#endif
     // ---------------- routing phase (warp 0 of rank 0) ----------------
     if (rank == 0 && warp == 0) {
       int k = S.k;
       int synced = S.synced;
       double last_poll = S.last_poll;
       const double beta = isnan(I.beta_fixed) ? S.beta : I.beta_fixed;
+      if (I.balancer == SSB_BAL_RR || I.balancer == SSB_BAL_RANDOM) {
+        // round robin and random read no engine state (balancers.py:139-153): every arrival
+        // is routed in one phase, 32 at a time — lane i takes arrival k0+i: server (rr+i) mod n,
+        // or the i-th of 32 consecutive Generator.integers(n) draws (drawn in order by every
+        // lane, kept by lane i); lanes that share a server append to its list in arrival
+        // order (match_any + rank in group)
+        for (int k0 = k; k0 < N; k0 += 32) {
+          const int kk = k0 + lane;
+          const bool valid = kk < N;
+          const double t = valid ? __ddiv_rn(arr[kk], I.qps_factor) : 0.0;
+          const int pr = valid ? prm[kk] : 0;
+          int s = (int)((rr + lane) % n);
+          if (I.balancer == SSB_BAL_RANDOM) {
+            const int m = N - k0 < 32 ? (int)(N - k0) : 32;
+            for (int j = 0; j < m; ++j) {
+              const int d = rng.integers(n);
+              if (j == lane) s = d;
+            }
+          }
+          const unsigned grp = __match_any_sync(FULL, valid ? s : -1);
+          const int before = __popc(grp & lanemask_lt());
+          const bool leader = before == 0;
+          const int base = valid ? cnt[s] : 0;
+          __syncwarp();
+          if (valid) {
+            int* rl = (int*)(scratch + I.scratch_offset + (long long)s * L.total + L.rl);
+            rl[base + before] = kk;
+            rec_srv[kk] = s;
+            atomicAdd((unsigned long long*)&rps[s], (unsigned long long)(long long)pr);
+            if (leader) {
+              cnt[s] = base + __popc(grp);
+              if (t < s_nb[s]) s_nb[s] = t;  // the group's earliest arrival
+            }
+          }
+          __syncwarp();
+          rr += N - k0 < 32 ? N - k0 : 32;
+        }
+        k = (int)N;
+      }
+      // p2c / sal: one arrival at a time (each route may read the view);
+      // the arrivals' times and prompts are fetched 32 at a time (lane i holds c0 + i)
+      int c0 = -64;
+      double c_t = 0.0;
+      int c_pr = 0;
       while (k < N) {
-        const double t = __ddiv_rn(arr[k], I.qps_factor);
-        const int pr = prm[k];
+        if (k >= c0 + 32) {
+          c0 = k;
+          const int kk = k + lane;
+          c_t = kk < N ? __ddiv_rn(arr[kk], I.qps_factor) : __longlong_as_double(0x7ff0000000000000LL);
+          c_pr = kk < N ? prm[kk] : 0;
+        }
+        const double t = __shfl_sync(FULL, c_t, k - c0);
+        const int pr = __shfl_sync(FULL, c_pr, k - c0);
         if (uses_view && __dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
           if (!synced) break;
           // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
@@ -462,10 +518,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
           if (lane == 0) S.polls += 1;
         }
         int s = 0;
-        if (I.balancer == SSB_BAL_RR) {  // balancers.py:139-142
-          s = (int)(rr % n);
-          rr++;
-        } else if (I.balancer == SSB_BAL_RANDOM) {  // :152-153
+        if (I.balancer == SSB_BAL_RANDOM) {  // :152-153
           s = rng.integers(n);
         } else if (I.balancer == SSB_BAL_P2C) {  // :167-176
           if (n > 1) {
@@ -475,50 +528,40 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
             s = v_if[j] < v_if[i] ? j : i;
           }
         } else {  // SAL (:204-212)
-          if (est_beta && !synced) {
-            // beta (balancers.py:96-100) moves with completions the routing warp has not
-            // seen; the route needs it only if the argmin can depend on it. A server with
-            // free_mem >= prompt has load == its queue term Q (beta*(prompt-free) <= 0 < Q);
-            // one with free_mem < prompt has load >= Q for every beta. So if the best
-            // unconstrained (Q, index) beats every constrained server's (Q, index), it wins
-            // for every beta and no barrier is needed.
-            double bu = 0.0, bc = 0.0;
-            int iu = 0x7fffffff, ic = 0x7fffffff;
-            for (int q = lane; q < n; q += 32) {
-              const double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
-                                          : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
-              if (v_f[q] < pr) { if (ic == 0x7fffffff || que < bc) { bc = que; ic = q; } }
-              else if (iu == 0x7fffffff || que < bu) { bu = que; iu = q; }
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-              const double ou = __shfl_xor_sync(FULL, bu, o), oc = __shfl_xor_sync(FULL, bc, o);
-              const int jou = __shfl_xor_sync(FULL, iu, o), joc = __shfl_xor_sync(FULL, ic, o);
-              if (jou != 0x7fffffff && (iu == 0x7fffffff || ou < bu || (ou == bu && jou < iu))) { bu = ou; iu = jou; }
-              if (joc != 0x7fffffff && (ic == 0x7fffffff || oc < bc || (oc == bc && joc < ic))) { bc = oc; ic = joc; }
-            }
-            const bool indep = ic == 0x7fffffff || (iu != 0x7fffffff && (bu < bc || (bu == bc && iu < ic)));
-            if (!indep) break;
-          }
-          double best = 0.0;
-          int bi = 0x7fffffff;
+          // per server (lane q, q+32, ...): the queue term Q = (queued+prompt)/cap (exact
+          // integers < 2^53; a power-of-two cap divides exactly as a product with 2^-k),
+          // the load max(beta*(prompt-free), Q) (sal_load, balancers.py:103-112) and whether
+          // the server is memory-constrained (free < prompt); each lane keeps its best
+          // (value, server) per quantity, then REDUX picks the warp minimum and the lowest
+          // server index among the lanes holding it (min(range(n), key=...) tie rule, :210)
+          unsigned long long kl = ~0ULL, ku = ~0ULL, kc = ~0ULL;
+          int sl = 0x7fffffff, su = 0x7fffffff, sc = 0x7fffffff;
           for (int q = lane; q < n; q += 32) {
-            // sal_load (balancers.py:103-112)
-            double mem = __dmul_rn(beta, (double)((long long)pr - v_f[q]));
-            // (queued + prompt) / cap: exact integers (< 2^53); for a power-of-two cap the
-            // correctly rounded quotient is the exact product with 2^-k
-            double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
-                                  : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
-            double load = que > mem ? que : mem;
-            if (bi == 0x7fffffff || load < best) { best = load; bi = q; }
+            const double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
+                                        : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
+            const double mem = __dmul_rn(beta, (double)((long long)pr - v_f[q]));
+            const double load = que > mem ? que : mem;
+            const unsigned long long k1 = dkey(load), kq = dkey(que);
+            if (k1 < kl) { kl = k1; sl = q; }  // q ascending: ties keep the lower server
+            if (v_f[q] < pr) { if (kq < kc) { kc = kq; sc = q; } }
+            else if (kq < ku) { ku = kq; su = q; }
           }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            double ob = __shfl_xor_sync(FULL, best, o);
-            int oi = __shfl_xor_sync(FULL, bi, o);
-            if (oi != 0x7fffffff && (bi == 0x7fffffff || ob < best || (ob == best && oi < bi))) { best = ob; bi = oi; }
+          if (est_beta && !synced) {
+            // beta moves with completions the routing warp has not seen; a server with
+            // free >= prompt has load == Q (beta*(prompt-free) <= 0 < Q), a constrained one
+            // load >= Q for every beta: if the best unconstrained (Q, server) beats every
+            // constrained one, the argmin is the same for every beta and no barrier is needed
+            const unsigned long long mc = warp_min_u64(kc);
+            if (mc != ~0ULL) {
+              const unsigned long long mu = warp_min_u64(ku);
+              const int iu = mu == ~0ULL ? 0x7fffffff : (int)__reduce_min_sync(FULL, ku == mu ? (unsigned)su : 0x7fffffffu);
+              const int ic = (int)__reduce_min_sync(FULL, kc == mc ? (unsigned)sc : 0x7fffffffu);
+              const bool indep = mu != ~0ULL && (mu < mc || (mu == mc && iu < ic));
+              if (!indep) break;
+            }
           }
-          s = bi;
+          const unsigned long long ml = warp_min_u64(kl);
+          s = (int)__reduce_min_sync(FULL, kl == ml ? (unsigned)sl : 0x7fffffffu);
           if (lane == 0) {  // note_routed (balancers.py:59-64)
             v_q[s] += pr;
             long long f = v_f[s] - pr;
@@ -537,7 +580,9 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
         }
         __syncwarp();
         k++;
-        if (!(k < N && __ddiv_rn(arr[k], I.qps_factor) == t)) synced = 0;  // equal times need no sync
+        double tn = __longlong_as_double(0x7ff0000000000000LL);
+        if (k < N) tn = (k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : __ddiv_rn(arr[k], I.qps_factor);
+        if (!(k < N && tn == t)) synced = 0;  // equal times need no sync
       }
       if (lane == 0) {
         S.k = k;
@@ -546,7 +591,13 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
         S.t_lim = k < N ? __ddiv_rn(arr[k], I.qps_factor) : __longlong_as_double(0x7ff0000000000000LL);
       }
     }
+#ifdef SSB_EPOCH_PROBE
+    const long long pt1 = clock64();
+#endif
     csync();
+#ifdef SSB_EPOCH_PROBE
+    const long long pt2 = clock64();
+#endif
     // ---------------- advance phase: every replica to its boundaries < t_lim ----------------
     const double t_lim = S.t_lim;
     long long dc = 0, di = 0, dout = 0;  // this warp's completions (beta sums)
@@ -573,7 +624,15 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
       atomicAdd((unsigned long long*)&S.fin_in, (unsigned long long)di);
       atomicAdd((unsigned long long*)&S.fin_out, (unsigned long long)dout);
     }
+#ifdef SSB_EPOCH_PROBE
+    const long long pt3 = clock64();
+#endif
     csync();
+#ifdef SSB_EPOCH_PROBE
+    if (rank == 0 && threadIdx.x == 0) {
+      pr_route += pt1 - pt0; pr_sync += (pt2 - pt1) + (clock64() - pt3); pr_adv_own += pt3 - pt2;
+    }
+#endif
     // ---------------- sync point: fold beta (on_finish, cluster.py:153-154) ----------------
     if (rank == 0 && threadIdx.x == 0) {
       if (est_beta)  // balancers.py:96-100 over every engine's completions so far
@@ -614,6 +673,8 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
 #ifdef SSB_EPOCH_PROBE
     out._pad = S.epochs;
     out.device_cycles = S.polls;
+    printf("EPOCHS inst %d servers %d epochs %d: route %lld cyc, warp0 advance %lld cyc, barrier wait (incl. slowest warp) %lld cyc\n",
+           idx, n, S.epochs, pr_route, pr_adv_own, pr_sync);
 #endif
     stats[idx] = out;
     if (ev_count) ev_count[idx] = evn;
