@@ -207,6 +207,7 @@ __device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restri
                                           int* __restrict__ r_gen, int* __restrict__ r_pfd, int* __restrict__ r_st, int R) {
   const int lane = threadIdx.x & 31;
   int out = 0;
+  #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
   for (int base = 0; base < R; base += 32) {
     const int j = base + lane;
     const bool valid = j < R;
@@ -499,6 +500,7 @@ struct Eng {
       }
       if (trail) {  // sorted by (remaining, id): insert in arrival order
         const int out = ok ? output[rid] : 0;
+        #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
         for (unsigned mm = m; mm; mm &= mm - 1) {
           const int b = __ffs(mm) - 1;
           trail_insert(__shfl_sync(FULL, rid, b), __shfl_sync(FULL, pr, b), __shfl_sync(FULL, out, b));
@@ -545,6 +547,7 @@ struct Eng {
     __syncwarp();
   }
   __device__ void flush_pushes() {
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int i = 0; i < nq; ++i) {
       const int rid_flag = p.v_idx[i], alloc = p.v_rem[i], key = (int)p.v_cum[i];
       if (st.W + 1 > cfg.Wc) { st.status = SSB_E_CAPACITY; break; }
@@ -582,6 +585,7 @@ struct Eng {
       if (need0 > limit) return 0;
     }
     int D = 0, used = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < st.W; base += 32) {
       int k = base + lane;
       bool valid = k < st.W;
@@ -660,6 +664,7 @@ struct Eng {
       double emin = 1e300;  // (first scan) certification bounds, see below
       int pmax = 0;
       const double qld = (double)ql;
+      #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
       for (int k0 = 0; k0 < st.W; k0 += 64) {  // two independent elements per lane per trip
         LKey x[2];
         bool hx[2];
@@ -748,6 +753,7 @@ struct Eng {
   // A taken (marked) victim's key becomes 0, which no later query or extraction matches.
   __device__ int victims_build(unsigned long long& vk, int& vb) {
     int V = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < st.R; base += 32) {
       const int j = base + lane;
       bool e = false;
@@ -775,6 +781,7 @@ struct Eng {
   __device__ __forceinline__ long long victims_gain(int V, unsigned long long vk, int vb, int b) const {
     if (V <= 32) return redux_add((int)(vk >> 32) > b ? vb : 0);
     long long t = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < V; base += 32) {
       const int i = base + lane;
       const unsigned long long k = i < V ? p.v_key[i] : 0ULL;
@@ -794,6 +801,7 @@ struct Eng {
     }
     unsigned long long best = 0;
     int bpos = -1;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int i = lane; i < V; i += 32) {
       const unsigned long long k = p.v_key[i];
       if ((int)(k >> 32) > b && k > best) { best = k; bpos = i; }
@@ -896,11 +904,13 @@ struct Eng {
 
   // ---- remove dispatched entries (physical slots in l_a[0..nd)) from an unordered waiting set ----
   __device__ void remove_dispatched_unordered(int nd) {
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int i = lane; i < nd; i += 32) p.w_rid[p.l_a[i]] = -1;
     __syncwarp();
     int Wn = st.W - nd;
     // holes: dispatched slots at logical position < Wn ; movers: kept entries at logical >= Wn
     int nh = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < nd; base += 32) {
       int i = base + lane;
       bool h = false;
@@ -916,6 +926,7 @@ struct Eng {
     }
     __syncwarp();
     int nm = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = Wn; base < st.W; base += 32) {
       int k = base + lane;
       bool mv = false;
@@ -948,6 +959,7 @@ struct Eng {
     int need_sum = 0;
     long long pend_sum = 0;
     int res_sum = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < nd; base += 32) {
       int j = base + lane;
       bool valid = j < nd;
@@ -1001,6 +1013,7 @@ struct Eng {
     int budget = cap - n_dec_plan;
     int dec_seen = 0, pf_used = 0, npf_ = 0;
     long long res = 0;
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < st.R; base += 32) {
       int j = base + lane;
       bool valid = j < st.R;
@@ -1145,6 +1158,7 @@ struct Eng {
       __syncwarp();
       // _evict_for_blocks: youngest dispatch first (table order descending), skipping the grower
       int needed = fext;  // blocks(new) - allocated_blocks(r)
+      #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
       for (int base = ((st.R - 1) >> 5) << 5; base >= 0 && st.free_blocks < needed; base -= 32) {
         int v = base + lane;
         bool live = v < st.R && v != j && p.r_st[v] != ST_GONE;
@@ -1188,6 +1202,7 @@ struct Eng {
   __device__ bool progress(int npf) {
     bool removed = false;
     // prefill chunks in plan order (table indices listed in l_b)
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < npf; base += 32) {
       int i = base + lane;
       int j = i < npf ? p.l_b[i] : 0;
@@ -1198,6 +1213,7 @@ struct Eng {
 #endif
     }
     // then decode tokens in plan order
+    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
     for (int base = 0; base < st.R; base += 32) {
       int j = base + lane;
       bool in = j < st.R && p.r_plan[j] == 1;
