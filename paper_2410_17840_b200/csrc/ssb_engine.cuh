@@ -201,6 +201,41 @@ __device__ __noinline__ void write_event(ssb_event* ev, long long pos, long long
   }
 }
 
+// One warp-uniform batch of events: lane i contributes code_a if bit i of mask_a, then code_b
+// if bit i of mask_b; order = lane order (a before b within a lane). Folds them into the
+// decision digest h (FNV-1a) and, with an event ring, writes them from position pos0.
+// Out of line: one copy for every emit site (the engine is instruction-fetch bound).
+__device__ __noinline__ unsigned long long emit_events(unsigned long long h, unsigned mask_a, int code_a,
+                                                       unsigned mask_b, int code_b, int rid_lane, double t,
+                                                       ssb_event* ev, long long pos0, long long cap, int server) {
+  const int lane = threadIdx.x & 31;
+  const unsigned both = mask_a | mask_b;
+  if (ev != nullptr && ((both >> lane) & 1u)) {
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    long long pos = pos0 + __popc(mask_a & lt) + __popc(mask_b & lt);
+    if ((mask_a >> lane) & 1u) write_event(ev, pos++, cap, t, rid_lane, server, code_a);
+    if ((mask_b >> lane) & 1u) write_event(ev, pos, cap, t, rid_lane, server, code_b);
+  }
+  unsigned m = both;
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1;
+    const int rid = __shfl_sync(FULL, rid_lane, b);
+    if ((mask_a >> b) & 1u) {
+      h ^= (unsigned long long)code_a; h *= FNV_PRIME;
+      h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
+      h ^= (unsigned long long)__double_as_longlong(t); h *= FNV_PRIME;
+    }
+    if ((mask_b >> b) & 1u) {
+      h ^= (unsigned long long)code_b; h *= FNV_PRIME;
+      h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
+      h ^= (unsigned long long)__double_as_longlong(t); h *= FNV_PRIME;
+    }
+  }
+  return h;
+}
+
 // stable compaction of a running table (drops ST_GONE entries); returns the new size.
 // Out of line with pointer/int arguments only, so callers keep their state in registers.
 __device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restrict__ r_prompt, int* __restrict__ r_out,
@@ -337,33 +372,13 @@ struct Eng {
     if (ev != nullptr) write_event(ev, pos, ev_cap, st.clock, rid, server, code);
   }
   // one event per lane in `mask`, lane order (warp-uniform call)
-  __device__ void emit(unsigned mask, int code, int rid_lane) {
-    if (ev != nullptr && ((mask >> lane) & 1u)) log_at(st.ev_n + __popc(mask & lanemask_lt()), code, rid_lane);
-    unsigned m = mask;
-    while (m) {
-      int b = __ffs(m) - 1;
-      m &= m - 1;
-      fold(code, __shfl_sync(FULL, rid_lane, b));
-    }
+  __device__ __forceinline__ void emit(unsigned mask, int code, int rid_lane) {
+    st.digest = emit_events(st.digest, mask, code, 0u, 0, rid_lane, st.clock, ev, st.ev_n, ev_cap, server);
     st.ev_n += __popc(mask);
   }
   // first_token (mask_a) then finish (mask_b) per lane, lanes in order
-  __device__ void emit2(unsigned mask_a, int code_a, unsigned mask_b, int code_b, int rid_lane) {
-    unsigned both = mask_a | mask_b;
-    if (ev != nullptr && ((both >> lane) & 1u)) {
-      unsigned lt = lanemask_lt();
-      long long pos = st.ev_n + __popc(mask_a & lt) + __popc(mask_b & lt);
-      if ((mask_a >> lane) & 1u) log_at(pos++, code_a, rid_lane);
-      if ((mask_b >> lane) & 1u) log_at(pos, code_b, rid_lane);
-    }
-    unsigned m = both;
-    while (m) {
-      int b = __ffs(m) - 1;
-      m &= m - 1;
-      int rid = __shfl_sync(FULL, rid_lane, b);
-      if ((mask_a >> b) & 1u) fold(code_a, rid);
-      if ((mask_b >> b) & 1u) fold(code_b, rid);
-    }
+  __device__ __forceinline__ void emit2(unsigned mask_a, int code_a, unsigned mask_b, int code_b, int rid_lane) {
+    st.digest = emit_events(st.digest, mask_a, code_a, mask_b, code_b, rid_lane, st.clock, ev, st.ev_n, ev_cap, server);
     st.ev_n += __popc(mask_a) + __popc(mask_b);
   }
   __device__ __forceinline__ void emit1(int code, int rid) {  // uniform single event
@@ -1156,23 +1171,35 @@ struct Eng {
       if (PREFILL && lane == 0) p.r_pfd[j] = ff2;  // the chunk landed before the grow
       if (PREFILL) st.pf_pend -= (long long)(ff2 - __shfl_sync(FULL, f, fl));
       __syncwarp();
-      // _evict_for_blocks: youngest dispatch first (table order descending), skipping the grower
-      int needed = fext;  // blocks(new) - allocated_blocks(r)
-      #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
-      for (int base = ((st.R - 1) >> 5) << 5; base >= 0 && st.free_blocks < needed; base -= 32) {
-        int v = base + lane;
-        bool live = v < st.R && v != j && p.r_st[v] != ST_GONE;
-        unsigned ml = __ballot_sync(FULL, live);
-        while (ml && st.free_blocks < needed) {
-          int b = 31 - __clz(ml);
-          ml &= ~(1u << b);
-          int vj = base + b;
-          int vs = p.r_st[vj];
-          int vrid = p.r_rid[vj], vpr = p.r_prompt[vj], vout = p.r_out[vj], vg = p.r_gen[vj], vf = p.r_pfd[vj];
-          preempt_entry(vj, vrid, vpr, vout, vg, vf, vs, SSB_EV_PREEMPT);
+      // _evict_for_blocks: youngest dispatch first (table order descending), skipping the grower,
+      // until the grow fits; if nothing is left to evict, park the grower itself (engine.py:
+      // 403-412). One preempt_entry call site for both (a smaller hot loop).
+      const int needed = fext;  // blocks(new) - allocated_blocks(r)
+      int vbase = ((st.R - 1) >> 5) << 5;
+      unsigned ml = 0;
+      bool parked = false;
+      #pragma unroll 1
+      while (st.free_blocks < needed) {
+        while (ml == 0 && vbase >= 0) {
+          const int v = vbase + lane;
+          ml = __ballot_sync(FULL, v < st.R && v != j && p.r_st[v] != ST_GONE);
+          if (ml == 0) vbase -= 32;
         }
+        int vj = j, code = SSB_EV_PARK;
+        if (ml != 0) {
+          const int b = 31 - __clz(ml);
+          ml &= ~(1u << b);
+          vj = vbase + b;
+          code = SSB_EV_PREEMPT;
+          if (ml == 0) vbase -= 32;
+        } else {
+          parked = true;
+        }
+        // (the grower's table entry already holds ff2 / fg / its state, see above)
+        preempt_entry(vj, p.r_rid[vj], p.r_prompt[vj], p.r_out[vj], p.r_gen[vj], p.r_pfd[vj], p.r_st[vj], code);
+        if (parked) break;
       }
-      if (st.free_blocks >= needed) {  // retry succeeds
+      if (!parked) {  // retry succeeds
         st.free_blocks -= fext;
         if (PREFILL) {
           if (lane == 0) { p.r_gen[j] = 1; rec_ft[frid] = st.clock; p.r_st[j] = ffin ? ST_GONE : ST_DECODE; }
@@ -1190,8 +1217,6 @@ struct Eng {
           st.finished += 1; st.fin_cnt += 1; st.fin_in += fpr; st.fin_out += fout;
           if (cfg.policy == SSB_POLICY_NOPREEMPT) st.committed -= wkey_for(fpr, fout, 0);
         }
-      } else {  // park: the grower alone exceeds the pool (engine.py:403-412)
-        preempt_entry(j, frid, fpr, fout, fg, ff2, PREFILL ? ST_PREFILL : ST_DECODE, SSB_EV_PARK);
       }
       __syncwarp();
       start = fl + 1;
