@@ -679,34 +679,23 @@ struct Eng {
       double emin = 1e300;  // (first scan) certification bounds, see below
       int pmax = 0;
       const double qld = (double)ql;
-      #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
-      for (int k0 = 0; k0 < st.W; k0 += 64) {  // two independent elements per lane per trip
-        LKey x[2];
-        bool hx[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k = k0 + 32 * u + lane;
-          hx[u] = k < st.W;
-          if (hx[u]) {
-            const int pos = phys(k);
-            x[u].rid = p.w_rid[pos] & 0x7fffffff;
-            x[u].enq = p.w_enq[pos];
-            x[u].k = k;
-            const int pend = p.w_pend[pos];
-            emin = fmin(emin, x[u].enq);
-            pmax = max(pmax, pend);
-            // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending; the
-            // int product is < 2^53 (queue_len < 2^31, pending <= max_context), so the
-            // binary64 product of the two exact operands is exact, as Python's int is
-            x[u].sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, x[u].enq)), __dmul_rn(qld, (double)pend));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (!hx[u] || (have_last && !lbetter(last, x[u]))) continue;  // only keys strictly after `last`
-          if (!h1 || lbetter(x[u], b1)) { b2 = b1; h2 = h1; b1 = x[u]; h1 = true; }
-          else if (!h2 || lbetter(x[u], b2)) { b2 = x[u]; h2 = true; }
-        }
+      #pragma unroll 1  // one element per lane per trip: the smallest loop body (instruction-fetch bound)
+      for (int k = lane; k < st.W; k += 32) {  // (lanes diverge only in their last trip)
+        LKey x;
+        const int pos = phys(k);
+        x.rid = p.w_rid[pos] & 0x7fffffff;
+        x.enq = p.w_enq[pos];
+        x.k = k;
+        const int pend = p.w_pend[pos];
+        emin = fmin(emin, x.enq);
+        pmax = max(pmax, pend);
+        // larry_score (policies.py:215-224): alpha*(clock-enq) - queue_len*pending; the
+        // int product is < 2^53 (queue_len < 2^31, pending <= max_context), so the
+        // binary64 product of the two exact operands is exact, as Python's int is
+        x.sc = __dsub_rn(__dmul_rn(cfg.alpha, __dsub_rn(st.clock, x.enq)), __dmul_rn(qld, (double)pend));
+        if (have_last && !lbetter(last, x)) continue;  // only keys strictly after `last`
+        if (!h1 || lbetter(x, b1)) { b2 = b1; h2 = h1; b1 = x; h1 = true; }
+        else if (!h2 || lbetter(x, b2)) { b2 = x; h2 = true; }
       }
       const unsigned w1 = larry_argmax(b1, h1);
       if (w1 == 0u) break;
