@@ -1057,13 +1057,9 @@ struct Eng {
   // (exclusive scan of released-minus-grown blocks); every lane before the first
   // failing grow commits in parallel; the failing one runs the serial eviction
   // cascade (_grow_or_evict / _evict_for_blocks) and the chunk restarts after it.
-#ifdef SSB_PROGRESS_TEMPLATE
-  template <bool PREFILL>
-  __device__ void progress_group(int j_lane, bool in_group, bool& removed_any) {
-#else
-  // one body for both sections (runtime flag): halves this cold path's instruction footprint
+  // one body for both sections (runtime flag, one call site in progress()): this path's
+  // instruction footprint matters more than the flag's cost
   __device__ void progress_group(const bool PREFILL, int j_lane, bool in_group, bool& removed_any) {
-#endif
     int start = 0;
     while (true) {
       int rid = 0, pr = 0, out = 0, g = 0, f = 0, s = ST_GONE, plan = 0;
@@ -1215,27 +1211,20 @@ struct Eng {
 
   __device__ bool progress(int npf) {
     bool removed = false;
-    // prefill chunks in plan order (table indices listed in l_b)
-    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
-    for (int base = 0; base < npf; base += 32) {
-      int i = base + lane;
-      int j = i < npf ? p.l_b[i] : 0;
-#ifdef SSB_PROGRESS_TEMPLATE
-      progress_group<true>(j, i < npf, removed);
-#else
-      progress_group(true, j, i < npf, removed);
-#endif
-    }
-    // then decode tokens in plan order
-    #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
-    for (int base = 0; base < st.R; base += 32) {
-      int j = base + lane;
-      bool in = j < st.R && p.r_plan[j] == 1;
-#ifdef SSB_PROGRESS_TEMPLATE
-      progress_group<false>(j, in, removed);
-#else
-      progress_group(false, j, in, removed);
-#endif
+    // prefill chunks in plan order (table indices listed in l_b), then decode tokens in plan
+    // order; ONE call site of progress_group for both sections (it is inlined: two sites
+    // would be two copies of the largest function in the hot loop)
+    #pragma unroll 1
+    for (int sec = 0; sec < 2; ++sec) {
+      const bool pre = sec == 0;
+      const int n = pre ? npf : st.R;
+      #pragma unroll 1  // chunk loops run 1-2 trips: keep the hot code small (instruction-fetch bound)
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const int j = pre ? (i < npf ? p.l_b[i] : 0) : i;
+        const bool in = pre ? i < npf : (i < st.R && p.r_plan[i] == 1);
+        progress_group(pre, j, in, removed);
+      }
     }
     if (nq) flush_pushes();
     return removed;
@@ -1247,7 +1236,10 @@ struct Eng {
   // commit need no memory round trip in between. When the plan's total grow
   // demand exceeds the free pool (rare: memory pressure) it hands over to the
   // general ordered path (progress_group) with the plan written to memory.
-  __device__ void batch_progress_small() {
+  // returns -1 when the iteration completed in registers, else the number of prefill plan
+  // entries for the ordered general path (plan in memory, clock already advanced; total_out =
+  // the batch's tokens) — step() runs that path from its single call site of progress()
+  __device__ int batch_progress_small(int& total_out) {
     const int cap = cfg.cap;
     const bool valid = lane < st.R;
     int s = ST_GONE, pr = 0, out = 0, g = 0, f = 0, rid = 0;
@@ -1269,7 +1261,7 @@ struct Eng {
     const int resident = redux_add(in_dec ? pr + g : (in_pf ? f : 0));  // engine.py:217-218
     const int pf_tokens = redux_add(chunk);
     const int total = n_dec_plan + pf_tokens;
-    if (total == 0) { st.status = SSB_E_STALL; return; }  // engine.py:209-214
+    if (total == 0) { st.status = SSB_E_STALL; return -1; }  // engine.py:209-214
     st.rsteps += __popc(m_dec) + __popc(m_pf);
     st.btokens += total;
     {  // iteration_latency (costmodel.py:45-47); clock += latency (engine.py:219-220)
@@ -1294,11 +1286,8 @@ struct Eng {
 #ifdef SSB_PHASE_TIMING
       tc[14] += 1;
 #endif
-      bool removed = progress(__popc(m_pf));
-      if (removed) compact_running();
-      if (total > st.peak) st.peak = total;
-      st.iterations += 1;
-      return;
+      total_out = total;
+      return __popc(m_pf);
     }
     const bool fin = (first && out == 1) || (in_dec && g + 1 == out);
     const int rel = fin ? (first ? blocks(pr + 1) : blocks(pr + g + 1)) : 0;
@@ -1340,6 +1329,7 @@ struct Eng {
     __syncwarp();
     if (total > st.peak) st.peak = total;
     st.iterations += 1;
+    return -1;
   }
 
   // ---- steady-state decode iteration (engine.py:300-357 specialised) ----
@@ -1495,19 +1485,24 @@ struct Eng {
       if (fast_decode()) { SSB_T1(bat, 3) return; }
     }
     drop_regs();
-    if (st.R <= 32) { batch_progress_small(); SSB_T1(bat, 4) return; }
-    int total, nent, npf;
-    long long resident;
-    form_batch(total, resident, nent, npf);
-    if (total == 0) { st.status = SSB_E_STALL; return; }  // engine.py:209-214
-    st.rsteps += nent;
-    st.btokens += total;
-    // iteration_latency (costmodel.py:45-47) then clock += latency (engine.py:219-220)
-    double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, (double)resident));
-    double comp = __dmul_rn(cfg.compute, (double)total);
-    double lat = __dadd_rn(cfg.overhead, comp > mem ? comp : mem);
-    st.clock = __dadd_rn(st.clock, lat);
-    bool removed = progress(npf);
+    int total = 0, npf;
+    if (st.R <= 32) {
+      npf = batch_progress_small(total);
+      if (npf < 0) { SSB_T1(bat, 4) return; }
+    } else {
+      int nent;
+      long long resident;
+      form_batch(total, resident, nent, npf);
+      if (total == 0) { st.status = SSB_E_STALL; return; }  // engine.py:209-214
+      st.rsteps += nent;
+      st.btokens += total;
+      // iteration_latency (costmodel.py:45-47) then clock += latency (engine.py:219-220)
+      double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, (double)resident));
+      double comp = __dmul_rn(cfg.compute, (double)total);
+      double lat = __dadd_rn(cfg.overhead, comp > mem ? comp : mem);
+      st.clock = __dadd_rn(st.clock, lat);
+    }
+    bool removed = progress(npf);  // the ordered general path: one call site
     if (removed) compact_running();
     if (total > st.peak) st.peak = total;
     st.iterations += 1;
