@@ -1226,8 +1226,7 @@ struct Eng {
         progress_group(pre, j, in, removed);
       }
     }
-    if (nq) flush_pushes();
-    return removed;
+    return removed;  // (queued waiting pushes are flushed by advance() after the step)
   }
 
   // ---- fused _form_batch + latency + _apply_progress for R <= 32 ----
@@ -1469,8 +1468,7 @@ struct Eng {
             vf = p.r_pfd[j];
         preempt_entry(j, vrid, vpr, vout, vg, vf, vs, SSB_EV_PREEMPT);
       }
-      flush_pushes();
-      compact_running();
+      compact_running();  // (their waiting pushes are flushed by advance() after the step)
       SSB_T1(pre, 13)
     }
     if (nd > 0) {
@@ -1540,6 +1538,9 @@ struct Eng {
         next_t = next_arrival(n_avail);
       }
       step();
+      // preempted / evicted / parked requests go back to the waiting set here, in the order
+      // they were queued (policy preempts, then grow evictions): one call site for every path
+      if (nq) flush_pushes();
       if (regs_ok && nodisp && st.status == SSB_OK && cfg.bs_shift >= 0)
         fast_forward(next_t < t_lim ? next_t : t_lim);
     }
