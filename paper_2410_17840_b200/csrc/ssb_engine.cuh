@@ -418,25 +418,33 @@ struct Eng {
     const unsigned fb = __shfl_sync(FULL, bits, f);
     return 4 * f + __ffs(fb) - 1;
   }
-  // first bucket >= b0 whose minimum need is <= T, or -1
+  // first bucket >= b0 whose minimum need is <= T, or -1. Climb from b0's chunk until a
+  // node <= T follows it, then descend (some child of a node <= T is <= T). One loop with a
+  // single chunk probe: the probe is inlined once (the engine is instruction-fetch bound).
   __device__ int t_find(int b0, int T) const {
     if (b0 >= cfg.tg.nb) return -1;
-    int lvl = 0, idx = b0, node = -1;
+    int lvl = 0, idx = b0, base = b0 & ~(TF - 1), lo = b0 & (TF - 1);
+    bool down = false;
+    #pragma unroll 1
     while (true) {
-      const int base = idx & ~(TF - 1);
-      const int r = t_chunk_first(t_off(lvl) + base, lvl == 0 ? (idx & (TF - 1)) : (idx & (TF - 1)) + 1, T);
-      if (r >= 0) { node = base + r; break; }
+      const int r = t_chunk_first(t_off(lvl) + base, lo, T);
+      if (down || r >= 0) {  // (descending, r >= 0 always holds)
+        const int node = base + r;
+        if (lvl == 0) return node;
+        down = true;
+        lvl -= 1;
+        base = node << TF_SHIFT;
+        lo = 0;
+        continue;
+      }
       if (lvl == cfg.tg.top) return -1;
       idx >>= TF_SHIFT;
       lvl += 1;
+      base = idx & ~(TF - 1);
+      lo = (idx & (TF - 1)) + 1;
     }
-    while (lvl > 0) {  // descend: some child of a node <= T is <= T
-      lvl -= 1;
-      const int base = node << TF_SHIFT;
-      node = base + t_chunk_first(t_off(lvl) + base, 0, T);
-    }
-    return node;
   }
+
   // set bucket b's minimum and restore "node = min of children" up the tree
   __device__ void t_set_leaf(int b, int val) {
     if (p.t_lv[b] == val) return;
