@@ -786,14 +786,9 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   // The longest trail_plus instances (the critical path of a sweep) get SMs of their own
   // with one CTA (4 warps): trail_plus is instruction-fetch bound, so 4 warps keep the
   // SM's throughput while each instance runs faster than among 8 (profiles/).
-  // Default: a quarter of trail_plus's SM share when it has >= 8 instances per reserved warp
-  // (C4: 22 SMs for the 88 longest of 1,024; measured 227 -> 220-222 ms, tools/probe_heavy.py).
+  // Off by default: it paid (227 -> 220 ms on C4) while trail_plus was instruction-fetch bound
+  // at 8 warps/SM; after the code-size work 8 warps win (166 vs 171-175 ms, tools/probe_heavy.py).
   int heavy_sms = 0;
-  {
-    const double share = total_work > 0 ? gwork[SSB_POLICY_TRAIL_PLUS] / total_work : 0.0;
-    heavy_sms = (int)(0.25 * share * sms_tab + 0.5);
-    if ((long long)sg[SSB_POLICY_TRAIL_PLUS].size() < 8LL * heavy_sms * ENGINE_WARPS_PER_CTA) heavy_sms = 0;
-  }
   if (const char* e = getenv("SSB_HEAVY_SMS")) heavy_sms = std::max(0, atoi(e));  // experiments
   heavy_sms = std::min<int>(heavy_sms, (int)sg[SSB_POLICY_TRAIL_PLUS].size() / ENGINE_WARPS_PER_CTA);
   heavy_sms = std::min(heavy_sms, sms_tab / 2);
