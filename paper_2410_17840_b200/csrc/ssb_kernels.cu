@@ -252,7 +252,10 @@ struct EngineQueues {
   int off[5];    // offset of each queue's order list in order[]
 };
 constexpr int Q_HEAVY = 4;
-__global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA, 1)
+#ifndef SSB_ENGINE_MIN_CTAS
+#define SSB_ENGINE_MIN_CTAS 1
+#endif
+__global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA, SSB_ENGINE_MIN_CTAS)
 k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, EngineQueues qs,
           int* __restrict__ queue, const unsigned char* __restrict__ sm_policy, int n_sm_policy,
           int* __restrict__ sm_slot, ssb_trace tr, ssb_records rec,
