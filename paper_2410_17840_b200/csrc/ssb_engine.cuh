@@ -183,13 +183,13 @@ __device__ __forceinline__ unsigned warp_argmin_u64(unsigned long long key, bool
 
 
 // FNV-1a over the 64-bit words (code, request id, time bits) of one event
-__device__ __noinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
+__device__ __forceinline__ unsigned long long fnv_event(unsigned long long h, int code, int rid, double t) {
   h ^= (unsigned long long)code; h *= FNV_PRIME;
   h ^= (unsigned long long)(long long)rid; h *= FNV_PRIME;
   h ^= (unsigned long long)__double_as_longlong(t); h *= FNV_PRIME;
   return h;
 }
-__device__ __noinline__ void write_event(ssb_event* ev, long long pos, long long cap, double t, int rid, int server,
+__device__ __forceinline__ void write_event(ssb_event* ev, long long pos, long long cap, double t, int rid, int server,
                                          int code) {
   if (pos < cap) {
     ssb_event e;
@@ -204,8 +204,9 @@ __device__ __noinline__ void write_event(ssb_event* ev, long long pos, long long
 // One warp-uniform batch of events: lane i contributes code_a if bit i of mask_a, then code_b
 // if bit i of mask_b; order = lane order (a before b within a lane). Folds them into the
 // decision digest h (FNV-1a) and, with an event ring, writes them from position pos0.
-// Out of line: one copy for every emit site (the engine is instruction-fetch bound).
-__device__ __noinline__ unsigned long long emit_events(unsigned long long h, unsigned mask_a, int code_a,
+// Inlined like every engine helper: a call in a hot function costs more than its code size
+// (measured: out-of-line helpers forced register save/restore around the calls).
+__device__ __forceinline__ unsigned long long emit_events(unsigned long long h, unsigned mask_a, int code_a,
                                                        unsigned mask_b, int code_b, int rid_lane, double t,
                                                        ssb_event* ev, long long pos0, long long cap, int server) {
   const int lane = threadIdx.x & 31;
@@ -237,8 +238,8 @@ __device__ __noinline__ unsigned long long emit_events(unsigned long long h, uns
 }
 
 // stable compaction of a running table (drops ST_GONE entries); returns the new size.
-// Out of line with pointer/int arguments only, so callers keep their state in registers.
-__device__ __noinline__ int compact_table(int* __restrict__ r_rid, int* __restrict__ r_prompt, int* __restrict__ r_out,
+// (Inlined: see emit_events.)
+__device__ __forceinline__ int compact_table(int* __restrict__ r_rid, int* __restrict__ r_prompt, int* __restrict__ r_out,
                                           int* __restrict__ r_gen, int* __restrict__ r_pfd, int* __restrict__ r_st, int R) {
   const int lane = threadIdx.x & 31;
   int out = 0;
