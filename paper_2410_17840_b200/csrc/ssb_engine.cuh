@@ -356,7 +356,7 @@ struct Eng {
     return x >= cfg.Wc ? x - cfg.Wc : x;
   }
   __device__ __forceinline__ double arrival_of(int rid) const {
-    return __ddiv_rn(arrival[rid], cfg.qps);  // scale_qps (workload.py:193)
+    return arrival[rid];  // already scaled by qps_factor (k_scale_arrivals, workload.py:193)
   }
   __device__ __forceinline__ int wkey_for(int prompt_len, int out, int gen) const {
     if (cfg.policy == SSB_POLICY_NOPREEMPT) {  // policies.py:116-117 reservation, in blocks

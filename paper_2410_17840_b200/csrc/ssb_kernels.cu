@@ -65,6 +65,19 @@ __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long l
   return L;
 }
 
+// Arrival times of an instance as the engines read them: the trace itself when qps_factor is
+// 1, else the instance's scaled copy (arrival / qps_factor, workload.py:193 scale_qps) that
+// k_scale_arrivals writes into its scratch after the servers' regions — so no binary64
+// division (a subroutine call on sm_100a) sits in the engine's hot loop.
+__host__ __device__ inline long long scaled_arrivals_offset(const ssb_instance& I, const Layout& L) {
+  return I.scratch_offset + L.total * (long long)(I.n_servers > 0 ? I.n_servers : 1);
+}
+__device__ inline const double* instance_arrivals(const ssb_instance& I, const Layout& L, ssb_trace tr,
+                                                  unsigned char* scratch) {
+  return I.qps_factor == 1.0 ? tr.arrival + I.trace_offset
+                             : (const double*)(scratch + scaled_arrivals_offset(I, L));
+}
+
 __device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
   SrvPtr p;
   p.w_enq = (double*)(base + L.w_enq);
@@ -155,7 +168,7 @@ __device__ inline void bind_engine(Eng& E, const ssb_instance& I, const Cfg& cfg
     E.p.l_c = sm_tab + 15 * RS;
     if (E.cfg.Rc > RS) E.cfg.Rc = RS;  // overflow -> SSB_E_CAPACITY -> host re-runs with global tables
   }
-  E.arrival = tr.arrival + I.trace_offset;
+  E.arrival = instance_arrivals(I, L, tr, scratch);
   E.prompt = tr.prompt + I.trace_offset;
   E.output = tr.output + I.trace_offset;
   E.rec_ft = rec.first_token + I.record_offset;
@@ -191,6 +204,23 @@ __device__ inline void clear_records(const Eng& E, long long N, int lane_base, i
     E.rec_fd[i] = __longlong_as_double(0x7ff8000000000000LL);
     E.rec_pc[i] = 0;
     E.rec_srv[i] = -1;
+  }
+}
+
+// ------------------------------------------------------------------------
+// scale_qps (workload.py:187-194) fused into the launch: arrival / qps_factor once per
+// request of every instance with a factor != 1 (IEEE division == Python's float division),
+// one CTA per instance, coalesced
+// ------------------------------------------------------------------------
+__global__ void k_scale_arrivals(const ssb_instance* __restrict__ inst, int n_inst, ssb_trace tr,
+                                 unsigned char* __restrict__ scratch) {
+  for (int i = blockIdx.x; i < n_inst; i += gridDim.x) {
+    const ssb_instance I = inst[i];
+    if (I.qps_factor == 1.0) continue;
+    const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+    double* out = (double*)(scratch + scaled_arrivals_offset(I, L));
+    const double* in = tr.arrival + I.trace_offset;
+    for (long long k = threadIdx.x; k < I.n_requests; k += blockDim.x) out[k] = __ddiv_rn(in[k], I.qps_factor);
   }
 }
 
@@ -436,7 +466,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   rng.shi = I.pcg_state_hi; rng.slo = I.pcg_state_lo; rng.ihi = I.pcg_inc_hi; rng.ilo = I.pcg_inc_lo;
   rng.has = 0; rng.buf = 0;
   long long rr = 0;
-  const double* arr = tr.arrival + I.trace_offset;
+  const double* arr = instance_arrivals(I, L, tr, scratch);  // already divided by qps_factor
   const int* prm = tr.prompt + I.trace_offset;
   int* rec_srv = rec.server + I.record_offset;
   const double poll = I.poll_interval_s;
@@ -463,7 +493,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
         for (int k0 = k; k0 < N; k0 += 32) {
           const int kk = k0 + lane;
           const bool valid = kk < N;
-          const double t = valid ? __ddiv_rn(arr[kk], I.qps_factor) : 0.0;
+          const double t = valid ? arr[kk] : 0.0;
           const int pr = valid ? prm[kk] : 0;
           int s = (int)((rr + lane) % n);
           if (I.balancer == SSB_BAL_RANDOM) {
@@ -502,7 +532,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
         if (k >= c0 + 32) {
           c0 = k;
           const int kk = k + lane;
-          c_t = kk < N ? __ddiv_rn(arr[kk], I.qps_factor) : __longlong_as_double(0x7ff0000000000000LL);
+          c_t = kk < N ? arr[kk] : __longlong_as_double(0x7ff0000000000000LL);
           c_pr = kk < N ? prm[kk] : 0;
         }
         const double t = __shfl_sync(FULL, c_t, k - c0);
@@ -584,14 +614,14 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
         __syncwarp();
         k++;
         double tn = __longlong_as_double(0x7ff0000000000000LL);
-        if (k < N) tn = (k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : __ddiv_rn(arr[k], I.qps_factor);
+        if (k < N) tn = (k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : arr[k];
         if (!(k < N && tn == t)) synced = 0;  // equal times need no sync
       }
       if (lane == 0) {
         S.k = k;
         S.synced = synced;
         S.last_poll = last_poll;
-        S.t_lim = k < N ? __ddiv_rn(arr[k], I.qps_factor) : __longlong_as_double(0x7ff0000000000000LL);
+        S.t_lim = k < N ? arr[k] : __longlong_as_double(0x7ff0000000000000LL);
       }
     }
 #ifdef SSB_EPOCH_PROBE
@@ -733,6 +763,7 @@ extern "C" size_t ssb_prepare(ssb_instance* h, int32_t n_inst) {
     I.scratch_offset = off;
     Layout L = make_layout(Wc, Rc, N, I.n_servers, I.engine);
     off += L.total * (long long)std::max(1, I.n_servers);
+    if (I.qps_factor != 1.0) off += align_up(8 * N, 256);  // scaled arrival times
   }
   return (size_t)off;
 }
@@ -761,7 +792,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
         std::min<long long>(I.engine.max_context, (long long)I.engine.pool_blocks * I.engine.block_size) >= (1LL << 20))
       return SSB_E_ARG;  // remaining-output buckets: 3 tree levels (2^20 buckets) at most
     Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
-    need = std::max(need, I.scratch_offset + L.total * (long long)I.n_servers);
+    need = std::max(need, scaled_arrivals_offset(I, L) + (I.qps_factor != 1.0 ? 8 * I.n_requests : 0));
     if (I.n_servers == 1) singles.push_back(i); else { multis.push_back(i); max_servers = std::max(max_servers, I.n_servers); }
   }
   if ((long long)scratch_bytes < need) return SSB_E_ARG;
@@ -843,6 +874,12 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   if (cudaMemcpyAsync(scratch, hdr.data(), sizeof(int) * hdr.size(), cudaMemcpyHostToDevice, stream) != cudaSuccess)
     return SSB_E_CUDA;
   const int* d_hdr = (const int*)scratch;
+  bool any_scaled = false;
+  for (int i = 0; i < n_inst; ++i) any_scaled |= h_inst[i].qps_factor != 1.0;
+  if (any_scaled) {
+    k_scale_arrivals<<<(unsigned)std::min(n_inst, 8 * sms), 256, 0, stream>>>(d_inst, n_inst, trace, scratch);
+    if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
+  }
   if (!multis.empty()) {
     // one cluster of G CTAs x nw warps per instance: enough warps for one replica each (<= 64)
     const int nw = std::min(CLUSTER_MAX_WARPS, max_servers);

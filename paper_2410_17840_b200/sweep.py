@@ -72,7 +72,8 @@ class SweepRunner:
         self.d2h_bytes = self.p_stats.numel() + self.p_summary.numel()
         self.n_singles = int((h_inst["n_servers"] == 1).sum())
         self.n_multis = len(h_inst) - self.n_singles
-        self.sim_launches = int(self.n_singles > 0) + int(self.n_multis > 0)
+        self.sim_launches = (int(self.n_singles > 0) + int(self.n_multis > 0)
+                             + int(bool((h_inst["qps_factor"] != 1.0).any())))  # + k_scale_arrivals
         self.copy_inputs()
         torch.cuda.synchronize()
 
