@@ -24,7 +24,10 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int ENGINE_WARPS_PER_CTA = 4;
+#ifndef SSB_ENGINE_WARPS_PER_CTA
+#define SSB_ENGINE_WARPS_PER_CTA 4
+#endif
+constexpr int ENGINE_WARPS_PER_CTA = SSB_ENGINE_WARPS_PER_CTA;
 
 __host__ __device__ inline long long align_up(long long x, long long a) { return (x + a - 1) / a * a; }
 
