@@ -1,7 +1,8 @@
 """Larger BASELINE-shaped runs on the CUDA path vs the oracle (bit-exact), sized so
-each finishes in seconds: C5 (64-replica SAL and RR clusters) on its first 600 s
-(~134k requests per instance), C3 (tight pool, long tails, recompute-on-resume) on
-its first 20,000 s, and the full C4 sweep of one seed (256 instances). Plus
+each finishes in seconds: C1 and C2 at full size, C5 (64-replica SAL and RR clusters)
+on its first 600 s (~134k requests per instance), C3 (tight pool, long tails,
+recompute-on-resume) on its first 20,000 s, and the C4 sweep of one seed (256
+instances). (tools/full_configs.py runs all five at full size.) Plus
 size-independent properties at those sizes: every request finished exactly once,
 event-time ordering of the records, preemption counts consistent with the counters,
 and run-to-run determinism of the decision digests."""
@@ -81,3 +82,14 @@ def test_c4_seed_sweep_matches_oracle_and_is_deterministic():
     _check_vs_oracle(batch, rec, st)
     _, _, st2 = _run(jobs)
     assert np.array_equal(st["digest"], st2["digest"])
+
+
+def test_c1_and_c2_full_size_match_oracle():
+    """BASELINE configs 1 (10,058 requests, fcfs and larry on the 70B profile) and 2 (~100k requests,
+    8 replicas, rr / p2c / sal / random) at full size."""
+    from paper_2410_17840_b200 import configs as C
+
+    for jobs in (C.c1_jobs(), C.c2_jobs()):
+        batch, rec, st = _run(jobs)
+        _properties(batch, rec, st)
+        _check_vs_oracle(batch, rec, st)
