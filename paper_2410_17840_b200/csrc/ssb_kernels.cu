@@ -803,7 +803,8 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   // Singles: one persistent kernel, SMs partitioned by policy (see k_engines).
   // Multis: one CTA per instance.
   std::vector<int> sg[4];
-  for (int i : singles) sg[h_inst[i].engine.policy & 3].push_back(i);
+  const bool one_queue = getenv("SSB_ONE_QUEUE") != nullptr;  // experiments: no per-policy SM partition
+  for (int i : singles) sg[one_queue ? 0 : (h_inst[i].engine.policy & 3)].push_back(i);
   double gwork[4] = {0, 0, 0, 0}, total_work = 0;
   for (int p = 0; p < 4; ++p) {
     std::stable_sort(sg[p].begin(), sg[p].end(),
