@@ -280,11 +280,15 @@ __device__ __forceinline__ unsigned sm_id() {
 // proportion to each policy's estimated work); a warp serves the queue of its SM's policy,
 // longest estimated cost first, and steals from the other queues once its own is empty.
 // Keeping one policy per SM keeps the policy-specific code of each SM's warps the same.
+// Queues: 2 per policy (queue 2p + c: class c of policy p — small / large KV pools, see
+// ssb_simulate) and
+// queue Q_HEAVY for the longest trail_plus instances when SSB_HEAVY_SMS reserves SMs for them.
+constexpr int NQ = 9;
+constexpr int Q_HEAVY = 8;
 struct EngineQueues {
-  int n[5];      // instances per queue: 4 policies + (queue 4) the longest trail_plus instances
-  int off[5];    // offset of each queue's order list in order[]
+  int n[NQ];    // instances per queue
+  int off[NQ];  // offset of each queue's order list in order[]
 };
-constexpr int Q_HEAVY = 4;
 #ifndef SSB_ENGINE_MIN_CTAS
 #define SSB_ENGINE_MIN_CTAS 1
 #endif
@@ -305,15 +309,19 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
     __syncthreads();
     if (s_slot > 0) return;
   }
-  // queue order: own queue, then the others (the heavy queue last unless it is ours)
-  int seq[5], nseq = 0;
-  seq[nseq++] = first;
-  if (first == Q_HEAVY) seq[nseq++] = SSB_POLICY_TRAIL_PLUS;
-  for (int k = 1; k < 4; ++k) seq[nseq++] = ((first == Q_HEAVY ? SSB_POLICY_TRAIL_PLUS : first) + k) & 3;
-  if (first != Q_HEAVY) seq[nseq++] = Q_HEAVY;
-  int k = 0;
-  while (k < nseq) {
-    const int pol = seq[k];
+  // queue order: own queue, the other class of the same policy, the other policies, the heavy
+  // queue last (a heavy SM continues with trail_plus)
+  const int home = first == Q_HEAVY ? 2 * SSB_POLICY_TRAIL_PLUS : first;
+  int k = first == Q_HEAVY ? -1 : 0;
+  while (k < NQ) {
+    // k = -1: the heavy queue; 0: home; 1: home's other class; 2..7: the other policies; 8: heavy
+    int pol;
+    if (k < 0) pol = Q_HEAVY;
+    else if (k == 0) pol = home;
+    else if (k == 1) pol = home ^ 1;
+    else if (k < 8) pol = ((home & ~1) + k) & 7;
+    else pol = Q_HEAVY;
+    if (k == 8 && first == Q_HEAVY) break;
     int q = 0;
     if (lane == 0) q = atomicAdd(queue + pol, 1);
     q = __shfl_sync(FULL, q, 0);
@@ -802,11 +810,21 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   if (max_servers > 4096) return SSB_E_ARG;
   // Singles: one persistent kernel, SMs partitioned by policy (see k_engines).
   // Multis: one CTA per instance.
-  std::vector<int> sg[4];
+  std::vector<int> sg[8];
   const bool one_queue = getenv("SSB_ONE_QUEUE") != nullptr;  // experiments: no per-policy SM partition
-  for (int i : singles) sg[one_queue ? 0 : (h_inst[i].engine.policy & 3)].push_back(i);
-  double gwork[4] = {0, 0, 0, 0}, total_work = 0;
-  for (int p = 0; p < 4; ++p) {
+  // Each policy's instances form two classes by KV pool size: pools of more than 2^16 tokens
+  // run much larger batches (the R > 32 table paths) than small ones, so giving the two their
+  // own SMs keeps each SM's executed code smaller (C4: 146 -> 142 ms, SSB_SPLIT_POOL=<blocks>
+  // overrides the threshold; 0 = no split).
+  long long split_tokens = 1LL << 16;
+  if (const char* e = getenv("SSB_SPLIT_POOL")) split_tokens = (long long)atoi(e) * 16;
+  for (int i : singles) {
+    const long long pool_tokens = (long long)h_inst[i].engine.pool_blocks * h_inst[i].engine.block_size;
+    const int cls = split_tokens > 0 && pool_tokens > split_tokens ? 1 : 0;
+    sg[one_queue ? 0 : 2 * (h_inst[i].engine.policy & 3) + cls].push_back(i);
+  }
+  double gwork[8] = {0, 0, 0, 0, 0, 0, 0, 0}, total_work = 0;
+  for (int p = 0; p < 8; ++p) {
     std::stable_sort(sg[p].begin(), sg[p].end(),
                      [&](int a, int b) { return h_inst[a].est_cost > h_inst[b].est_cost; });
     for (int i : sg[p]) gwork[p] += (double)std::max(1, h_inst[i].est_cost);
@@ -828,13 +846,13 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   // at 8 warps/SM; after the code-size work 8 warps win (166 vs 171-175 ms, tools/probe_heavy.py).
   int heavy_sms = 0;
   if (const char* e = getenv("SSB_HEAVY_SMS")) heavy_sms = std::max(0, atoi(e));  // experiments
-  heavy_sms = std::min<int>(heavy_sms, (int)sg[SSB_POLICY_TRAIL_PLUS].size() / ENGINE_WARPS_PER_CTA);
+  heavy_sms = std::min<int>(heavy_sms, (int)sg[2 * SSB_POLICY_TRAIL_PLUS].size() / ENGINE_WARPS_PER_CTA);
   heavy_sms = std::min(heavy_sms, sms_tab / 2);
   const int n_heavy = heavy_sms * ENGINE_WARPS_PER_CTA;
-  std::vector<int> heavy(sg[SSB_POLICY_TRAIL_PLUS].begin(), sg[SSB_POLICY_TRAIL_PLUS].begin() + n_heavy);
-  sg[SSB_POLICY_TRAIL_PLUS].erase(sg[SSB_POLICY_TRAIL_PLUS].begin(), sg[SSB_POLICY_TRAIL_PLUS].begin() + n_heavy);
+  std::vector<int> heavy(sg[2 * SSB_POLICY_TRAIL_PLUS].begin(), sg[2 * SSB_POLICY_TRAIL_PLUS].begin() + n_heavy);
+  sg[2 * SSB_POLICY_TRAIL_PLUS].erase(sg[2 * SSB_POLICY_TRAIL_PLUS].begin(), sg[2 * SSB_POLICY_TRAIL_PLUS].begin() + n_heavy);
   total_work = 0;
-  for (int p = 0; p < 4; ++p) {
+  for (int p = 0; p < 8; ++p) {
     gwork[p] = 0;
     for (int i : sg[p]) gwork[p] += (double)std::max(1, h_inst[i].est_cost);
     total_work += gwork[p];
@@ -843,9 +861,9 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   unsigned char* smpol = (unsigned char*)(hdr.data() + 16);
   for (int k = 0; k < heavy_sms; ++k) smpol[sms_rest + k] = (unsigned char)Q_HEAVY;
   {  // SMs per policy in proportion to estimated work (largest remainder), >= 1 if it has work
-    int cnt[4] = {0, 0, 0, 0}, given = 0;
-    double rem[4];
-    for (int p = 0; p < 4; ++p) {
+    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, given = 0;
+    double rem[8];
+    for (int p = 0; p < 8; ++p) {
       const double want = total_work > 0 ? sms_rest * gwork[p] / total_work : 0.0;
       cnt[p] = sg[p].empty() ? 0 : std::max(1, (int)want);
       rem[p] = want - cnt[p];
@@ -853,22 +871,22 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     }
     while (given > sms_rest) {
       int pm = 0;
-      for (int p = 1; p < 4; ++p) if (cnt[p] > cnt[pm]) pm = p;
+      for (int p = 1; p < 8; ++p) if (cnt[p] > cnt[pm]) pm = p;
       cnt[pm]--; given--;
     }
     while (given < sms_rest) {
       int pm = -1;
-      for (int p = 0; p < 4; ++p) if (!sg[p].empty() && (pm < 0 || rem[p] > rem[pm])) pm = p;
+      for (int p = 0; p < 8; ++p) if (!sg[p].empty() && (pm < 0 || rem[p] > rem[pm])) pm = p;
       if (pm < 0) break;
       cnt[pm]++; rem[pm] -= 1.0; given++;
     }
     int s0 = 0;
-    for (int p = 0; p < 4; ++p) for (int k = 0; k < cnt[p] && s0 < sms_rest; ++k) smpol[s0++] = (unsigned char)p;
+    for (int p = 0; p < 8; ++p) for (int k = 0; k < cnt[p] && s0 < sms_rest; ++k) smpol[s0++] = (unsigned char)p;
     for (; s0 < sms_rest; ++s0) smpol[s0] = 0;
   }
   EngineQueues qs;
   int o = hdr0;
-  for (int p = 0; p < 4; ++p) { qs.off[p] = o - hdr0; qs.n[p] = (int)sg[p].size(); for (int i : sg[p]) hdr[o++] = i; }
+  for (int p = 0; p < 8; ++p) { qs.off[p] = o - hdr0; qs.n[p] = (int)sg[p].size(); for (int i : sg[p]) hdr[o++] = i; }
   qs.off[Q_HEAVY] = o - hdr0;
   qs.n[Q_HEAVY] = (int)heavy.size();
   for (int i : heavy) hdr[o++] = i;
