@@ -230,6 +230,10 @@ __global__ void k_scale_arrivals(const ssb_instance* __restrict__ inst, int n_in
 // ------------------------------------------------------------------------
 // single-server instances: one warp each, persistent
 // ------------------------------------------------------------------------
+// POL: the instance's policy as a compile-time constant, so the kernel holds one engine copy per
+// policy and an SM (which serves one policy at a time, see k_engines) executes only its copy:
+// a smaller hot code footprint and no policy branches in the loop.
+template <int POL>
 __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ inst, int idx, ssb_trace tr,
                                              ssb_records rec, ssb_stats* __restrict__ stats,
                                              unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
@@ -237,7 +241,8 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
   const int lane = lane_id();
   const long long t0 = clock64();
   const ssb_instance I = inst[idx];
-  const Cfg cfg = make_cfg(I);
+  Cfg cfg = make_cfg(I);
+  cfg.policy = POL;  // compile-time policy: this copy of the engine holds only POL's code
   const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
   Eng E;
   bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap, sm_tab);
@@ -285,6 +290,7 @@ __device__ __forceinline__ unsigned sm_id() {
 // queue Q_HEAVY for the longest trail_plus instances when SSB_HEAVY_SMS reserves SMs for them.
 constexpr int NQ = 9;
 constexpr int Q_HEAVY = 8;
+__device__ __forceinline__ bool known_sm(unsigned smid, int n_sm_policy) { return smid < (unsigned)n_sm_policy; }
 struct EngineQueues {
   int n[NQ];    // instances per queue
   int off[NQ];  // offset of each queue's order list in order[]
@@ -295,7 +301,7 @@ struct EngineQueues {
 __global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA, SSB_ENGINE_MIN_CTAS)
 k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, EngineQueues qs,
           int* __restrict__ queue, const unsigned char* __restrict__ sm_policy, int n_sm_policy,
-          int* __restrict__ sm_slot, ssb_trace tr, ssb_records rec,
+          int* __restrict__ sm_slot, int* __restrict__ sm_done, ssb_trace tr, ssb_records rec,
           ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
           int64_t* ev_count) {
   extern __shared__ int sm_engines[];
@@ -303,16 +309,15 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
   int* sm_tab = sm_engines + (threadIdx.x >> 5) * (SM_COLS * RS);  // this warp's running table
   const int lane = lane_id();
   const unsigned smid = sm_id();
-  const int first = smid < (unsigned)n_sm_policy ? sm_policy[smid] : 0;
-  if (first == Q_HEAVY) {  // SMs of the longest instances run one CTA (see ssb_simulate)
-    if (threadIdx.x == 0) s_slot = atomicAdd(sm_slot + smid, 1);
-    __syncthreads();
-    if (s_slot > 0) return;
-  }
+  const int first = known_sm(smid, n_sm_policy) ? sm_policy[smid] : 0;
+  if (threadIdx.x == 0) s_slot = known_sm(smid, n_sm_policy) ? atomicAdd(sm_slot + smid, 1) : 0;
+  __syncthreads();
+  if (first == Q_HEAVY && s_slot > 0) return;  // SMs of the longest instances run one CTA (see ssb_simulate)
   // queue order: own queue, the other class of the same policy, the other policies, the heavy
   // queue last (a heavy SM continues with trail_plus)
   const int home = first == Q_HEAVY ? 2 * SSB_POLICY_TRAIL_PLUS : first;
   int k = first == Q_HEAVY ? -1 : 0;
+  bool switched = false;
   while (k < NQ) {
     // k = -1: the heavy queue; 0: home; 1: home's other class; 2..7: the other policies; 8: heavy
     int pol;
@@ -322,6 +327,19 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
     else if (k < 8) pol = ((home & ~1) + k) & 7;
     else pol = Q_HEAVY;
     if (k == 8 && first == Q_HEAVY) break;
+    if (k == 2 && !switched && first != Q_HEAVY && known_sm(smid, n_sm_policy)) {
+      switched = true;
+      // The SM switches policy as a whole: a warp whose own policy is drained waits until every
+      // warp resident on this SM is, then all steal in the same order and so run the same
+      // policy's code (a warp running another policy's engine beside the home policy's warps
+      // would share the SM's instruction cache between two hot loops — measured slower).
+      if (lane == 0) {
+        atomicAdd(sm_done + smid, 1);
+        const int resident = *((volatile int*)(sm_slot + smid)) * (int)(blockDim.x >> 5);
+        while (*((volatile int*)(sm_done + smid)) < resident) __nanosleep(2000);
+      }
+      __syncwarp();
+    }
     int q = 0;
     if (lane == 0) q = atomicAdd(queue + pol, 1);
     q = __shfl_sync(FULL, q, 0);
@@ -329,7 +347,13 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
       k += 1;
       continue;
     }
-    run_instance(inst, order[qs.off[pol] + q], tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab);
+    const int idx = order[qs.off[pol] + q];
+    switch (inst[idx].engine.policy) {  // the instance's own policy (a queue may mix them: SSB_ONE_QUEUE)
+      case SSB_POLICY_FCFS: run_instance<SSB_POLICY_FCFS>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      case SSB_POLICY_NOPREEMPT: run_instance<SSB_POLICY_NOPREEMPT>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      case SSB_POLICY_TRAIL_PLUS: run_instance<SSB_POLICY_TRAIL_PLUS>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      default: run_instance<SSB_POLICY_LARRY>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+    }
   }
 }
 
@@ -733,7 +757,7 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
 // scheduling header of ssb_simulate: queue counters, per-SM policy table and CTA slot
 // counters (sized for up to MAX_SMS SMs), instance order lists
 constexpr int MAX_SMS = 1024;
-static long long header_bytes(int n_inst) { return align_up(4LL * (16 + (MAX_SMS + 3) / 4 + 4 + MAX_SMS) + 8LL * n_inst, 256); }
+static long long header_bytes(int n_inst) { return align_up(4LL * (16 + (MAX_SMS + 3) / 4 + 4 + 2 * MAX_SMS) + 8LL * n_inst, 256); }
 
 extern "C" int32_t ssb_abi_version(void) { return SSB_ABI_VERSION; }
 
@@ -837,7 +861,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   // header (ints): [queue counters x4, pad x12][sm policy table (bytes)][per-SM CTA slot
   // counters][singles by policy][multis]
   const int smtab_ints = (MAX_SMS + 3) / 4 + 4;
-  const int hdr0 = 16 + smtab_ints + MAX_SMS;
+  const int hdr0 = 16 + smtab_ints + 2 * MAX_SMS;  // + per-SM CTA slot counters + per-SM drained-warp counters
   std::vector<int> hdr(hdr0 + n_inst, 0);
   // The longest trail_plus instances (the critical path of a sweep) get SMs of their own
   // with one CTA (4 warps): trail_plus is instruction-fetch bound, so 4 warps keep the
@@ -937,7 +961,8 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const int grid = sms * std::max(1, occ);
     k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(
         d_inst, d_hdr + hdr0, qs, (int*)scratch, (const unsigned char*)(d_hdr + 16), sms_tab,
-        (int*)scratch + 16 + smtab_ints, trace, records, d_stats, scratch, d_events, event_cap, d_event_count);
+        (int*)scratch + 16 + smtab_ints, (int*)scratch + 16 + smtab_ints + MAX_SMS, trace, records, d_stats, scratch,
+        d_events, event_cap, d_event_count);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   return SSB_OK;
