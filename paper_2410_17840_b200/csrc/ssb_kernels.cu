@@ -336,7 +336,10 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
       if (lane == 0) {
         atomicAdd(sm_done + smid, 1);
         const int resident = *((volatile int*)(sm_slot + smid)) * (int)(blockDim.x >> 5);
-        while (*((volatile int*)(sm_done + smid)) < resident) __nanosleep(2000);
+#ifndef SSB_SWITCH_SLACK
+#define SSB_SWITCH_SLACK 0
+#endif
+        while (*((volatile int*)(sm_done + smid)) < resident - SSB_SWITCH_SLACK) __nanosleep(2000);
       }
       __syncwarp();
     }
