@@ -1522,7 +1522,7 @@ struct Eng {
     int rid = (cfg.n_servers == 1) ? st.next_arr : p.rl[st.next_arr];
     return arrival_of(rid);
   }
-  __device__ void advance(double t_lim, int n_avail) {
+  __device__ __forceinline__ void advance(double t_lim, int n_avail) {
 #ifdef SSB_PHASE_TIMING
     for (int i = 0; i < 16; ++i) tm[i] = tc[i] = 0;
 #endif

@@ -428,14 +428,17 @@ constexpr int CLUSTER_MAX_WARPS = 8;
 constexpr int CLUSTER_MAX_CTAS = 8;       // portable cluster size
 constexpr int CLUSTER_SMEM_SERVERS = 12;  // shared running tables per CTA (12 x 16 KiB)
 
-__global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr,
-                          ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch,
-                          ssb_event* events, long long ev_cap, int64_t* ev_count, int smem_tabs) {
+// The cluster body with the instance's policy as a compile-time constant (one engine copy per
+// policy, like k_engines); k_cluster dispatches on the instance's policy.
+template <int POL>
+__device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ inst, const int* __restrict__ order,
+                                             ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
+                                             unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
+                                             int64_t* ev_count, int smem_tabs, long long* smem_ll,
+                                             ClusterShared& S_own) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
-  extern __shared__ long long smem_ll[];
-  __shared__ ClusterShared S_own;
   const int idx = order[blockIdx.x / G];
   const ssb_instance I = inst[idx];
   const int n = I.n_servers;
@@ -460,7 +463,8 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   // cluster (<= 8 replicas) uses the cheaper CTA barrier
   auto csync = [&]() { if (G == 1) __syncthreads(); else cl.sync(); };
   auto tab_of = [&](int s) { return tabs_in_smem ? sm_tabs + ((s / GW) * nwarps + warp) * SM_COLS * RS : nullptr; };
-  const Cfg cfg = make_cfg(I);
+  Cfg cfg = make_cfg(I);
+  cfg.policy = POL;
   const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
 
@@ -749,6 +753,20 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
 #endif
     stats[idx] = out;
     if (ev_count) ev_count[idx] = evn;
+  }
+}
+
+__global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr,
+                          ssb_records rec, ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch,
+                          ssb_event* events, long long ev_cap, int64_t* ev_count, int smem_tabs) {
+  extern __shared__ long long smem_ll[];
+  __shared__ ClusterShared S_own;
+  const int G = (int)cg::this_cluster().num_blocks();
+  switch (inst[order[blockIdx.x / G]].engine.policy) {
+    case SSB_POLICY_FCFS: cluster_body<SSB_POLICY_FCFS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_tabs, smem_ll, S_own); break;
+    case SSB_POLICY_NOPREEMPT: cluster_body<SSB_POLICY_NOPREEMPT>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_tabs, smem_ll, S_own); break;
+    case SSB_POLICY_TRAIL_PLUS: cluster_body<SSB_POLICY_TRAIL_PLUS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_tabs, smem_ll, S_own); break;
+    default: cluster_body<SSB_POLICY_LARRY>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_tabs, smem_ll, S_own); break;
   }
 }
 
