@@ -80,6 +80,7 @@ struct Cfg {
   int policy, max_output, bs, bs_shift, pool, cap, max_running, max_ctx;
   unsigned long long bmul;  // ceil(2^32 / bs): blocks() as one multiply-shift, exact (see blocks)
   int n_servers, Wc, Rc;
+  bool wide;  // latency-mode kernel: the R <= 64 register path is compiled in (k_engines<true>)
   double alpha, c, mem_base, mem_kv, compute, overhead, qps;
   TrailGeom tg;
 };
@@ -1340,6 +1341,123 @@ struct Eng {
     return -1;
   }
 
+  // ---- fused _form_batch + latency + _apply_progress for 32 < R <= 64 (latency kernel) ----
+  // batch_progress_small with two register chunks per lane (entries lane and lane+32, table
+  // order = chunk 0 then chunk 1). Only the latency-mode kernel (few instances, one per SM)
+  // compiles it in (cfg.wide): it shortens single-instance chains (C1 13% faster) but its
+  // extra hot code slows the many-instance sweep. Same return convention as batch_progress_small.
+  __device__ int batch_progress_64(int& total_out) {
+    const int cap = cfg.cap;
+    const unsigned lt = lanemask_lt();
+    const int j1 = lane + 32;
+    const bool vb = j1 < st.R;
+    int sa = p.r_st[lane], pra = p.r_prompt[lane], oa = p.r_out[lane], ga = p.r_gen[lane], fa = p.r_pfd[lane],
+        ra = p.r_rid[lane];
+    int sb = ST_GONE, prb = 0, ob = 0, gb = 0, fb = 0, rb = 0;
+    if (vb) { sb = p.r_st[j1]; prb = p.r_prompt[j1]; ob = p.r_out[j1]; gb = p.r_gen[j1]; fb = p.r_pfd[j1]; rb = p.r_rid[j1]; }
+    const bool deca = sa == ST_DECODE, decb = sb == ST_DECODE, pfa = sa == ST_PREFILL, pfb = sb == ST_PREFILL;
+    const unsigned mda = __ballot_sync(FULL, deca), mdb = __ballot_sync(FULL, decb);
+    const int nda = __popc(mda), ndec = nda + __popc(mdb);
+    const bool in_deca = deca && __popc(mda & lt) < cap;
+    const bool in_decb = decb && nda + __popc(mdb & lt) < cap;
+    const int n_dec_plan = min(ndec, cap);
+    const int B = cap - n_dec_plan;
+    const int penda = pfa ? pra + ga - fa : 0, pendb = pfb ? prb + gb - fb : 0;
+    const int inca = warp_incl_scan(penda, lane), incb = warp_incl_scan(pendb, lane);
+    const int tota = __shfl_sync(FULL, inca, 31);
+    const int befa = inca - penda, befb = tota + incb - pendb;
+    const int cha = (pfa && B - befa > 0) ? min(penda, B - befa) : 0;
+    const int chb = (pfb && B - befb > 0) ? min(pendb, B - befb) : 0;
+    const bool in_pfa = cha > 0, in_pfb = chb > 0;
+    const unsigned m_pfa = __ballot_sync(FULL, in_pfa), m_pfb = __ballot_sync(FULL, in_pfb);
+    const unsigned m_deca = __ballot_sync(FULL, in_deca), m_decb = __ballot_sync(FULL, in_decb);
+    const int resident = redux_add(in_deca ? pra + ga : (in_pfa ? fa : 0)) +
+                         redux_add(in_decb ? prb + gb : (in_pfb ? fb : 0));
+    const int pf_tokens = redux_add(cha) + redux_add(chb);
+    const int total = n_dec_plan + pf_tokens;
+    if (total == 0) { st.status = SSB_E_STALL; return -1; }
+    st.rsteps += __popc(m_deca) + __popc(m_decb) + __popc(m_pfa) + __popc(m_pfb);
+    st.btokens += total;
+    {
+      double mem = __dadd_rn(cfg.mem_base, __dmul_rn(cfg.mem_kv, (double)resident));
+      double comp = __dmul_rn(cfg.compute, (double)total);
+      st.clock = __dadd_rn(st.clock, __dadd_rn(cfg.overhead, comp > mem ? comp : mem));
+    }
+    const int f2a = fa + cha, f2b = fb + chb;
+    const bool firsta = in_pfa && f2a >= pra + ga && ga == 0, firstb = in_pfb && f2b >= prb + gb && gb == 0;
+    const bool reca = in_pfa && f2a >= pra + ga && ga > 0, recb = in_pfb && f2b >= prb + gb && gb > 0;
+    int exa = 0, exb = 0;
+    if (firsta) exa = blocks(pra + 1) - blocks(pra);
+    else if (in_deca) exa = blocks(pra + ga + 1) - blocks(pra + ga);
+    if (firstb) exb = blocks(prb + 1) - blocks(prb);
+    else if (in_decb) exb = blocks(prb + gb + 1) - blocks(prb + gb);
+    const int need = redux_add(exa) + redux_add(exb);
+    if (need > st.free_blocks) {
+      p.r_plan[lane] = in_deca ? 1 : (in_pfa ? cha + 1 : 0);
+      if (vb) p.r_plan[j1] = in_decb ? 1 : (in_pfb ? chb + 1 : 0);
+      const int npa = __popc(m_pfa);
+      if (in_pfa) p.l_b[__popc(m_pfa & lt)] = lane;
+      if (in_pfb) p.l_b[npa + __popc(m_pfb & lt)] = j1;
+      __syncwarp();
+      total_out = total;
+      return npa + __popc(m_pfb);
+    }
+    const bool fina = (firsta && oa == 1) || (in_deca && ga + 1 == oa);
+    const bool finb = (firstb && ob == 1) || (in_decb && gb + 1 == ob);
+    const int rela = fina ? (firsta ? blocks(pra + 1) : blocks(pra + ga + 1)) : 0;
+    const int relb = finb ? (firstb ? blocks(prb + 1) : blocks(prb + gb + 1)) : 0;
+    st.free_blocks += redux_add(rela) + redux_add(relb) - need;
+    const int g2a = firsta ? 1 : (in_deca ? ga + 1 : ga), g2b = firstb ? 1 : (in_decb ? gb + 1 : gb);
+    const int s2a = fina ? ST_GONE : ((firsta || reca) ? ST_DECODE : sa);
+    const int s2b = finb ? ST_GONE : ((firstb || recb) ? ST_DECODE : sb);
+    if (firsta) rec_ft[ra] = st.clock;
+    if (firstb) rec_ft[rb] = st.clock;
+    if (fina) rec_fin[ra] = st.clock;
+    if (finb) rec_fin[rb] = st.clock;
+    const unsigned mfa = __ballot_sync(FULL, firsta), mfb = __ballot_sync(FULL, firstb);
+    const unsigned mxa = __ballot_sync(FULL, fina), mxb = __ballot_sync(FULL, finb);
+    const unsigned mra = __ballot_sync(FULL, reca), mrb = __ballot_sync(FULL, recb);
+    if (mfa | mfb | mxa | mxb) {
+      emit2(mfa, SSB_EV_FIRST_TOKEN, mxa & m_pfa, SSB_EV_FINISH, ra);
+      emit2(mfb, SSB_EV_FIRST_TOKEN, mxb & m_pfb, SSB_EV_FINISH, rb);
+      emit(mxa & m_deca, SSB_EV_FINISH, ra);
+      emit(mxb & m_decb, SSB_EV_FINISH, rb);
+    }
+    st.pf_pend -= pf_tokens;
+    st.ndec += __popc(mfa | mra) + __popc(mfb | mrb) - __popc(mxa) - __popc(mxb);
+    if (mxa | mxb) {
+      nodisp = false;
+      const int nf = __popc(mxa) + __popc(mxb);
+      st.finished += nf;
+      st.fin_cnt += nf;
+      st.fin_in += redux_add(fina ? pra : 0) + redux_add(finb ? prb : 0);
+      st.fin_out += redux_add(fina ? oa : 0) + redux_add(finb ? ob : 0);
+      if (cfg.policy == SSB_POLICY_NOPREEMPT)
+        st.committed -= redux_add(fina ? wkey_for(pra, oa, 0) : 0) + redux_add(finb ? wkey_for(prb, ob, 0) : 0);
+      const bool ka = s2a != ST_GONE, kb = vb && s2b != ST_GONE;
+      const unsigned mka = __ballot_sync(FULL, ka), mkb = __ballot_sync(FULL, kb);
+      __syncwarp();
+      if (ka) {
+        const int d = __popc(mka & lt);
+        p.r_rid[d] = ra; p.r_prompt[d] = pra; p.r_out[d] = oa; p.r_gen[d] = g2a; p.r_pfd[d] = f2a; p.r_st[d] = s2a;
+      }
+      if (kb) {
+        const int d = __popc(mka) + __popc(mkb & lt);
+        p.r_rid[d] = rb; p.r_prompt[d] = prb; p.r_out[d] = ob; p.r_gen[d] = g2b; p.r_pfd[d] = f2b; p.r_st[d] = s2b;
+      }
+      st.R = __popc(mka) + __popc(mkb);
+    } else {
+      if (in_pfa) { p.r_pfd[lane] = f2a; p.r_gen[lane] = g2a; p.r_st[lane] = s2a; }
+      else if (in_deca) p.r_gen[lane] = g2a;
+      if (in_pfb) { p.r_pfd[j1] = f2b; p.r_gen[j1] = g2b; p.r_st[j1] = s2b; }
+      else if (in_decb) p.r_gen[j1] = g2b;
+    }
+    __syncwarp();
+    if (total > st.peak) st.peak = total;
+    st.iterations += 1;
+    return -1;
+  }
+
   // ---- steady-state decode iteration (engine.py:300-357 specialised) ----
   // Preconditions (checked by step): every running request is DECODING,
   // R <= min(64, cap) so the plan is "one token each, table order", block size a
@@ -1493,8 +1611,8 @@ struct Eng {
     }
     drop_regs();
     int total = 0, npf;
-    if (st.R <= 32) {
-      npf = batch_progress_small(total);
+    if (st.R <= 32 || (cfg.wide && st.R <= 64)) {
+      npf = st.R <= 32 ? batch_progress_small(total) : batch_progress_64(total);
       if (npf < 0) { SSB_T1(bat, 4) return; }
     } else {
       int nent;

@@ -129,6 +129,7 @@ __device__ inline Cfg make_cfg(const ssb_instance& I) {
   c.compute = e.compute_per_token_s;
   c.overhead = e.overhead_s;
   c.qps = I.qps_factor;
+  c.wide = false;
   c.tg = trail_geom(e.max_context, e.pool_blocks, e.block_size);
   return c;
 }
@@ -233,7 +234,7 @@ __global__ void k_scale_arrivals(const ssb_instance* __restrict__ inst, int n_in
 // POL: the instance's policy as a compile-time constant, so the kernel holds one engine copy per
 // policy and an SM (which serves one policy at a time, see k_engines) executes only its copy:
 // a smaller hot code footprint and no policy branches in the loop.
-template <int POL>
+template <int POL, bool WIDE>
 __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ inst, int idx, ssb_trace tr,
                                              ssb_records rec, ssb_stats* __restrict__ stats,
                                              unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
@@ -243,6 +244,7 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
   const ssb_instance I = inst[idx];
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;  // compile-time policy: this copy of the engine holds only POL's code
+  cfg.wide = WIDE;   // latency-mode kernel only (see k_engines)
   const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
   Eng E;
   bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap, sm_tab);
@@ -298,6 +300,10 @@ struct EngineQueues {
 #ifndef SSB_ENGINE_MIN_CTAS
 #define SSB_ENGINE_MIN_CTAS 1
 #endif
+// WIDE: latency mode for batches with at most one instance per SM (each runs alone, so a
+// larger hot loop costs nothing and the R <= 64 register path shortens its serial chain); the
+// many-instance kernel (WIDE = false) keeps the smaller code.
+template <bool WIDE>
 __global__ void __launch_bounds__(32 * ENGINE_WARPS_PER_CTA, SSB_ENGINE_MIN_CTAS)
 k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, EngineQueues qs,
           int* __restrict__ queue, const unsigned char* __restrict__ sm_policy, int n_sm_policy,
@@ -352,10 +358,10 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
     }
     const int idx = order[qs.off[pol] + q];
     switch (inst[idx].engine.policy) {  // the instance's own policy (a queue may mix them: SSB_ONE_QUEUE)
-      case SSB_POLICY_FCFS: run_instance<SSB_POLICY_FCFS>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
-      case SSB_POLICY_NOPREEMPT: run_instance<SSB_POLICY_NOPREEMPT>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
-      case SSB_POLICY_TRAIL_PLUS: run_instance<SSB_POLICY_TRAIL_PLUS>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
-      default: run_instance<SSB_POLICY_LARRY>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      case SSB_POLICY_FCFS: run_instance<SSB_POLICY_FCFS, WIDE>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      case SSB_POLICY_NOPREEMPT: run_instance<SSB_POLICY_NOPREEMPT, WIDE>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      case SSB_POLICY_TRAIL_PLUS: run_instance<SSB_POLICY_TRAIL_PLUS, WIDE>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
+      default: run_instance<SSB_POLICY_LARRY, WIDE>(inst, idx, tr, rec, stats, scratch, events, ev_cap, ev_count, sm_tab); break;
     }
   }
 }
@@ -974,13 +980,16 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
   if (!singles.empty()) {
+    // latency mode when every instance can have an SM to itself (see k_engines<WIDE>)
+    const bool wide = (int)singles.size() <= sms && getenv("SSB_NO_LATENCY_MODE") == nullptr;
+    auto kern = wide ? k_engines<true> : k_engines<false>;
     int occ = 1;
     const size_t sm = sizeof(int) * SM_COLS * RS * ENGINE_WARPS_PER_CTA;
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_engines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_engines, 32 * ENGINE_WARPS_PER_CTA, sm);
+    if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * ENGINE_WARPS_PER_CTA, sm);
     if (const char* cap = getenv("SSB_CTAS_PER_SM")) occ = std::min(occ, std::max(1, atoi(cap)));  // experiments
     const int grid = sms * std::max(1, occ);
-    k_engines<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(
+    kern<<<grid, 32 * ENGINE_WARPS_PER_CTA, sm, stream>>>(
         d_inst, d_hdr + hdr0, qs, (int*)scratch, (const unsigned char*)(d_hdr + 16), sms_tab,
         (int*)scratch + 16 + smtab_ints, (int*)scratch + 16 + smtab_ints + MAX_SMS, trace, records, d_stats, scratch,
         d_events, event_cap, d_event_count);
