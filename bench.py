@@ -52,8 +52,10 @@ def config(world: int) -> dict:
         "parallelism": f"instance-sharded x{world}" + (" + NCCL all_gather of summaries" if world > 1 else ""),
         "l2": "working set (trace+records+scratch, ~1 GB per GPU) exceeds L2; L2 flushed (256 MB write) before "
               "every timed step",
-        "schedule": "per-policy persistent kernels sharing the GPU by estimated work, longest-first queues; "
-                    "estimates = device cycles of each instance measured in the untimed first pass",
+        "schedule": "one persistent kernel; SMs split among (policy, KV-pool class) queues by estimated work, one "
+                    "engine copy per policy, longest-first queues, an SM switches policy only when all its warps are "
+                    "drained; estimates = iterations x the policy's mean device cycles per iteration, measured in the "
+                    "untimed first pass",
     }
 
 
