@@ -609,6 +609,28 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
             s = v_if[j] < v_if[i] ? j : i;
           }
         } else {  // SAL (:204-212)
+          // fast path (cap a power of two, beta > 0, prompt > 0, every queued+prompt < 2^52): Q
+          // orders exactly as the integer queued+prompt, an unconstrained server's load is Q and
+          // a constrained one's is >= Q for every beta, so when the (Q, server) minimum is
+          // unconstrained it is the load argmin whatever beta is (no barrier needed either):
+          // one 64-bit warp minimum over (queued+prompt) << 12 | server (n <= 4096)
+          bool fast = false;
+          if (cap_pow2 && beta > 0.0 && pr > 0) {
+            unsigned long long kx = ~0ULL;
+            bool big = false;
+            for (int q = lane; q < n; q += 32) {
+              const unsigned long long X = (unsigned long long)(v_q[q] + pr);
+              big |= X >= (1ULL << 52);
+              const unsigned long long key = (X << 12) | (unsigned)q;
+              kx = key < kx ? key : kx;
+            }
+            if (!__any_sync(FULL, big)) {
+              const int w = (int)(warp_min_u64(kx) & 0xfffULL);
+              if (v_f[w] >= pr) { s = w; fast = true; }
+              else if (est_beta && !synced) break;  // a constrained server leads: beta decides
+            }
+          }
+          if (!fast) {
           // per server (lane q, q+32, ...): the queue term Q = (queued+prompt)/cap (exact
           // integers < 2^53; a power-of-two cap divides exactly as a product with 2^-k),
           // the load max(beta*(prompt-free), Q) (sal_load, balancers.py:103-112) and whether
@@ -643,6 +665,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           }
           const unsigned long long ml = warp_min_u64(kl);
           s = (int)__reduce_min_sync(FULL, kl == ml ? (unsigned)sl : 0x7fffffffu);
+          }
           if (lane == 0) {  // note_routed (balancers.py:59-64)
             v_q[s] += pr;
             long long f = v_f[s] - pr;
