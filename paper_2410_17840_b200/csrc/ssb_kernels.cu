@@ -528,6 +528,15 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
 #endif
     // ---------------- routing phase (warp 0 of rank 0) ----------------
     if (rank == 0 && warp == 0) {
+      // rank 0's own shared memory under the same names: plain shared loads/stores instead of
+      // the generic (DSMEM-capable) accesses the other ranks need
+      long long* const v_q = smem_ll;
+      long long* const v_f = smem_ll + n;
+      long long* const v_if = smem_ll + 2 * n;
+      long long* const rps = smem_ll + 3 * n;
+      int* const cnt = (int*)(smem_ll + 4 * n);
+      double* const s_nb = (double*)(smem_ll + 5 * ((n + 1) & ~1));
+      ClusterShared& S = S_own;
       int k = S.k;
       int synced = S.synced;
       double last_poll = S.last_poll;
