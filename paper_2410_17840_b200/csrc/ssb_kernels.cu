@@ -597,6 +597,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
         if (uses_view && __dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
           if (!synced) break;
           // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
+          #pragma unroll 1  // n <= 64 in practice: 1-2 trips, no unrolled remainder chain
           for (int s = lane; s < n; s += 32) {
             const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
             v_q[s] = sv->wpend_sum + (rps[s] - sv->enq_prompt_sum);
@@ -627,6 +628,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           if (cap_pow2 && beta > 0.0 && pr > 0) {
             unsigned long long kx = ~0ULL;
             bool big = false;
+            #pragma unroll 1  // n <= 64 in practice: 1-2 trips, no unrolled remainder chain
             for (int q = lane; q < n; q += 32) {
               const unsigned long long X = (unsigned long long)(v_q[q] + pr);
               big |= X >= (1ULL << 52);
@@ -648,6 +650,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           // server index among the lanes holding it (min(range(n), key=...) tie rule, :210)
           unsigned long long kl = ~0ULL, ku = ~0ULL, kc = ~0ULL;
           int sl = 0x7fffffff, su = 0x7fffffff, sc = 0x7fffffff;
+          #pragma unroll 1  // n <= 64 in practice: 1-2 trips, no unrolled remainder chain
           for (int q = lane; q < n; q += 32) {
             const double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
                                         : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
