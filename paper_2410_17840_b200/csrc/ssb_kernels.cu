@@ -678,15 +678,14 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           const unsigned long long ml = warp_min_u64(kl);
           s = (int)__reduce_min_sync(FULL, kl == ml ? (unsigned)sl : 0x7fffffffu);
           }
-          if (lane == 0) {  // note_routed (balancers.py:59-64)
+        }
+        if (lane == 0) {
+          if (I.balancer == SSB_BAL_SAL) {  // note_routed (balancers.py:59-64)
             v_q[s] += pr;
             long long f = v_f[s] - pr;
             v_f[s] = f > 0 ? f : 0;
             v_if[s] += 1;
           }
-          __syncwarp();
-        }
-        if (lane == 0) {
           int* rl = (int*)(scratch + I.scratch_offset + (long long)s * L.total + L.rl);
           rl[cnt[s]] = k;
           cnt[s] += 1;
