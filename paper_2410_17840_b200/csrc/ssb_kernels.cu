@@ -619,11 +619,11 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
             s = v_if[j] < v_if[i] ? j : i;
           }
         } else {  // SAL (:204-212)
-          // fast path (cap a power of two, beta > 0, prompt > 0, every queued+prompt < 2^52): Q
+          // fast path (cap a power of two, beta > 0, prompt > 0, every queued+prompt < 2^51): Q
           // orders exactly as the integer queued+prompt, an unconstrained server's load is Q and
           // a constrained one's is >= Q for every beta, so when the (Q, server) minimum is
           // unconstrained it is the load argmin whatever beta is (no barrier needed either):
-          // one 64-bit warp minimum over (queued+prompt) << 12 | server (n <= 4096)
+          // one 64-bit warp minimum over (queued+prompt) << 13 | server << 1 | constrained (n <= 4096)
           bool fast = false;
           if (cap_pow2 && beta > 0.0 && pr > 0) {
             unsigned long long kx = ~0ULL;
@@ -631,13 +631,14 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
             #pragma unroll 1  // n <= 64 in practice: 1-2 trips, no unrolled remainder chain
             for (int q = lane; q < n; q += 32) {
               const unsigned long long X = (unsigned long long)(v_q[q] + pr);
-              big |= X >= (1ULL << 52);
-              const unsigned long long key = (X << 12) | (unsigned)q;
+              big |= X >= (1ULL << 51);
+              // low bit: constrained (free < prompt); (X, q) is unique, so it never decides
+              const unsigned long long key = (X << 13) | ((unsigned)q << 1) | (unsigned)(v_f[q] < pr);
               kx = key < kx ? key : kx;
             }
             if (!__any_sync(FULL, big)) {
-              const int w = (int)(warp_min_u64(kx) & 0xfffULL);
-              if (v_f[w] >= pr) { s = w; fast = true; }
+              const unsigned long long m = warp_min_u64(kx);
+              if (!(m & 1ULL)) { s = (int)((m >> 1) & 0xfffULL); fast = true; }
               else if (est_beta && !synced) break;  // a constrained server leads: beta decides
             }
           }
@@ -699,11 +700,13 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
         if (k < N) tn = (k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : arr[k];
         if (!(k < N && tn == t)) synced = 0;  // equal times need no sync
       }
+      const double t_next = k >= N ? __longlong_as_double(0x7ff0000000000000LL)
+                          : (k >= c0 && k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : arr[k];
       if (lane == 0) {
         S.k = k;
         S.synced = synced;
         S.last_poll = last_poll;
-        S.t_lim = k < N ? arr[k] : __longlong_as_double(0x7ff0000000000000LL);
+        S.t_lim = t_next;
       }
     }
 #ifdef SSB_EPOCH_PROBE
