@@ -537,6 +537,17 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
       int* const cnt = (int*)(smem_ll + 4 * n);
       double* const s_nb = (double*)(smem_ll + 5 * ((n + 1) & ~1));
       ClusterShared& S = S_own;
+      // sync point: fold the completions of the advance phase that just ended into beta
+      // (on_finish, cluster.py:153-154; balancers.py:96-100) — here rather than behind a barrier
+      // of its own; the first pass folds nothing (beta stays the prior)
+      if (lane == 0) {
+        if (est_beta)
+          S.beta = S.fin_cnt == 0 ? I.beta_prior : __ddiv_rn((double)(S.fin_in + S.fin_out), (double)S.fin_out);
+        S.synced = 1;
+        S.epochs += 1;
+        if (S.k >= N || S.err) S.done = 1;
+      }
+      __syncwarp();
       int k = S.k;
       int synced = S.synced;
       double last_poll = S.last_poll;
@@ -716,6 +727,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
 #ifdef SSB_EPOCH_PROBE
     const long long pt2 = clock64();
 #endif
+    if (S.done) break;
     // ---------------- advance phase: every replica to its boundaries < t_lim ----------------
     const double t_lim = S.t_lim;
     long long dc = 0, di = 0, dout = 0;  // this warp's completions (beta sums)
@@ -751,16 +763,6 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
       pr_route += pt1 - pt0; pr_sync += (pt2 - pt1) + (clock64() - pt3); pr_adv_own += pt3 - pt2;
     }
 #endif
-    // ---------------- sync point: fold beta (on_finish, cluster.py:153-154) ----------------
-    if (rank == 0 && threadIdx.x == 0) {
-      if (est_beta)  // balancers.py:96-100 over every engine's completions so far
-        S.beta = S.fin_cnt == 0 ? I.beta_prior : __ddiv_rn((double)(S.fin_in + S.fin_out), (double)S.fin_out);
-      S.synced = 1;
-      S.epochs += 1;
-      if (S.k >= N || S.err) S.done = 1;
-    }
-    csync();
-    if (S.done) break;
   }
   csync();  // every CTA has read S.done: rank 0's shared memory may go away after this
 
