@@ -234,16 +234,17 @@ def cluster_unit_scenarios():
     return out
 
 
-def fuzz_cluster_scenarios(n=96, seed=31337, block_sizes=(4, 16), prefix="fuzzcl"):
+def fuzz_cluster_scenarios(n=96, seed=31337, block_sizes=(4, 16), prefix="fuzzcl", caps=(32, 256, 1024),
+                           betas=(1.0, 2.0, 6.5), bals=("rr", "random", "p2c", "sal")):
     """Randomised multi-replica instances: every balancer x policy, tight pools,
     poll intervals from 1 ms to inf, fixed and estimated beta, equal-time bursts."""
     rng = np.random.default_rng(seed)
     out = []
-    bals = ["rr", "random", "p2c", "sal"]
+    bals = list(bals)
     pols = ["fcfs", "nopreempt", "trail_plus", "larry"]
     for i in range(n):
-        b = bals[i % 4]
-        pol = pols[(i // 4) % 4]
+        b = bals[i % len(bals)]
+        pol = pols[(i // len(bals)) % 4]
         ns = int(rng.integers(2, 9))
         nreq = int(rng.integers(5, 150))
         if rng.random() < 0.3:
@@ -258,9 +259,9 @@ def fuzz_cluster_scenarios(n=96, seed=31337, block_sizes=(4, 16), prefix="fuzzcl
         if pol == "nopreempt":
             peak = max(peak, max(-(-min(8192, int(p) + max_out) // bs) for p in prompts))
         pool = peak + int(rng.integers(0, int(rng.choice([4, 40, 400, 4000]))))
-        cap = int(rng.choice([32, 256, 1024]))
+        cap = int(rng.choice(list(caps)))
         poll = float(rng.choice([0.001, 0.05, 0.1, 1.0, float("inf")]))
-        beta_fixed = None if rng.random() < 0.6 else float(rng.choice([1.0, 2.0, 6.5]))
+        beta_fixed = None if rng.random() < 0.6 else float(rng.choice(list(betas)))
         c = float(rng.choice([0.0, 0.5, 1.0])) if pol == "trail_plus" else 0.0
         tr = [(float(a), int(p), int(o)) for a, p, o in zip(arrivals, prompts, outputs)]
         out.append(scen(f"{prefix}_{b}_{pol}_{i}",
@@ -330,4 +331,9 @@ GROUPS = {
     # division there and the steady-state decode paths are off)
     "fuzz_odd_blocks": lambda: fuzz_engine_scenarios(80, seed=4242, block_sizes=(3, 5, 10, 12, 24), prefix="odd")
     + fuzz_cluster_scenarios(24, seed=4243, block_sizes=(3, 10, 24), prefix="oddcl"),
+    # sal / p2c routing off the integer-key fast path: token caps that are not powers of two
+    # (the queue term is a true division) beside power-of-two ones, fixed and estimated beta
+    "fuzz_route": lambda: fuzz_cluster_scenarios(48, seed=5151, block_sizes=(4, 16), prefix="route",
+                                                 caps=(48, 100, 1000, 1024), betas=(1.0, 1.25, 9.0),
+                                                 bals=("sal", "sal", "p2c")),
 }

@@ -11,7 +11,7 @@ from helpers import compare_instance, load_golden, scenario_batch
 
 pytestmark = pytest.mark.gpu
 
-GROUPS = ["engine_unit", "cluster_unit", "c2", "c3", "c6", "fuzz_engine", "fuzz_cluster", "fuzz_odd_blocks"]
+GROUPS = ["engine_unit", "cluster_unit", "c2", "c3", "c6", "fuzz_engine", "fuzz_cluster", "fuzz_odd_blocks", "fuzz_route"]
 
 
 def _sim():

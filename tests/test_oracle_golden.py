@@ -8,7 +8,7 @@ import scenarios as S
 from helpers import compare_instance, load_golden, scenario_batch
 from oracle import oracle as O
 
-GROUPS_FAST = ["engine_unit", "cluster_unit", "c2", "c3", "fuzz_engine", "fuzz_cluster", "c6", "fuzz_odd_blocks"]
+GROUPS_FAST = ["engine_unit", "cluster_unit", "c2", "c3", "fuzz_engine", "fuzz_cluster", "c6", "fuzz_odd_blocks", "fuzz_route"]
 
 
 @pytest.fixture(scope="module", autouse=True)
