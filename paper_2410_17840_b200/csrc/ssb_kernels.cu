@@ -434,6 +434,8 @@ constexpr int CLUSTER_MAX_WARPS = 8;
 constexpr int CLUSTER_MAX_CTAS = 8;       // portable cluster size
 constexpr int CLUSTER_SMEM_SERVERS = 12;  // shared running tables per CTA (12 x 16 KiB)
 
+template <int B> struct BalTag { static constexpr int value = B; };
+
 // The cluster body with the instance's policy as a compile-time constant (one engine copy per
 // policy, like k_engines); k_cluster dispatches on the instance's policy.
 template <int POL>
@@ -506,7 +508,6 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
   }
   csync();
 
-  const bool uses_view = I.balancer == SSB_BAL_P2C || I.balancer == SSB_BAL_SAL;
   const bool est_beta = I.balancer == SSB_BAL_SAL && isnan(I.beta_fixed);
   const bool cap_pow2 = cfg.cap > 0 && (cfg.cap & (cfg.cap - 1)) == 0;
   const double inv_cap = cap_pow2 ? __ddiv_rn(1.0, (double)cfg.cap) : 0.0;
@@ -596,6 +597,10 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
       int c0 = -64;
       double c_t = 0.0;
       int c_pr = 0;
+      // one copy of the per-arrival loop per balancer (no balancer branches inside it); random
+      // and round robin never get here (routed above)
+      auto route_loop = [&](auto bal_tag) {
+      constexpr int BAL = decltype(bal_tag)::value;
       while (k < N) {
         if (k >= c0 + 32) {
           c0 = k;
@@ -605,7 +610,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
         }
         const double t = __shfl_sync(FULL, c_t, k - c0);
         const int pr = __shfl_sync(FULL, c_pr, k - c0);
-        if (uses_view && __dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
+        if (__dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
           if (!synced) break;
           // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
           #pragma unroll 1  // n <= 64 in practice: 1-2 trips, no unrolled remainder chain
@@ -620,9 +625,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           if (lane == 0) S.polls += 1;
         }
         int s = 0;
-        if (I.balancer == SSB_BAL_RANDOM) {  // :152-153
-          s = rng.integers(n);
-        } else if (I.balancer == SSB_BAL_P2C) {  // :167-176
+        if constexpr (BAL == SSB_BAL_P2C) {  // :167-176
           if (n > 1) {
             int i = rng.integers(n);
             int j = rng.integers(n - 1);
@@ -692,7 +695,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           }
         }
         if (lane == 0) {
-          if (I.balancer == SSB_BAL_SAL) {  // note_routed (balancers.py:59-64)
+          if constexpr (BAL == SSB_BAL_SAL) {  // note_routed (balancers.py:59-64)
             v_q[s] += pr;
             long long f = v_f[s] - pr;
             v_f[s] = f > 0 ? f : 0;
@@ -711,6 +714,9 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
         if (k < N) tn = (k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : arr[k];
         if (!(k < N && tn == t)) synced = 0;  // equal times need no sync
       }
+      };
+      if (I.balancer == SSB_BAL_SAL) route_loop(BalTag<SSB_BAL_SAL>{});
+      else if (I.balancer == SSB_BAL_P2C) route_loop(BalTag<SSB_BAL_P2C>{});
       const double t_next = k >= N ? __longlong_as_double(0x7ff0000000000000LL)
                           : (k >= c0 && k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : arr[k];
       if (lane == 0) {
