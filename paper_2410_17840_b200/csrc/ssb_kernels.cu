@@ -694,19 +694,25 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           s = (int)__reduce_min_sync(FULL, kl == ml ? (unsigned)sl : 0x7fffffffu);
           }
         }
-        if (lane == 0) {
-          if constexpr (BAL == SSB_BAL_SAL) {  // note_routed (balancers.py:59-64)
-            v_q[s] += pr;
-            long long f = v_f[s] - pr;
-            v_f[s] = f > 0 ? f : 0;
-            v_if[s] += 1;
-          }
+        // bookkeeping: every lane reads (one address: broadcast), lane 0 stores — predicated
+        // stores instead of a divergent lane-0 block on the routing chain
+        {
+          const bool w0 = lane == 0;
+          const int cs = cnt[s];
+          const long long rq = rps[s];
+          const double nb0 = s_nb[s];
           int* rl = (int*)(scratch + I.scratch_offset + (long long)s * L.total + L.rl);
-          rl[cnt[s]] = k;
-          cnt[s] += 1;
-          rps[s] += pr;
-          rec_srv[k] = s;
-          if (t < s_nb[s]) s_nb[s] = t;  // its boundary is max(t, clock) >= t
+          if constexpr (BAL == SSB_BAL_SAL) {  // note_routed (balancers.py:59-64)
+            const long long vq = v_q[s], vf = v_f[s] - pr, vi = v_if[s];
+            if (w0) v_q[s] = vq + pr;
+            if (w0) v_f[s] = vf > 0 ? vf : 0;
+            if (w0) v_if[s] = vi + 1;
+          }
+          if (w0) rl[cs] = k;
+          if (w0) cnt[s] = cs + 1;
+          if (w0) rps[s] = rq + pr;
+          if (w0) rec_srv[k] = s;
+          if (w0 && t < nb0) s_nb[s] = t;  // its boundary is max(t, clock) >= t
         }
         __syncwarp();
         k++;
