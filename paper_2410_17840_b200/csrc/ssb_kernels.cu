@@ -601,6 +601,9 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
       // and round robin never get here (routed above)
       auto route_loop = [&](auto bal_tag) {
       constexpr int BAL = decltype(bal_tag)::value;
+      // engines are synced to the phase's first arrival; they stay synced for the arrivals that
+      // share its time (no simulated time passes), not beyond
+      double t_prev = k < N ? arr[k] : 0.0;
       while (k < N) {
         if (k >= c0 + 32) {
           c0 = k;
@@ -610,6 +613,8 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
         }
         const double t = __shfl_sync(FULL, c_t, k - c0);
         const int pr = __shfl_sync(FULL, c_pr, k - c0);
+        synced = t == t_prev ? synced : 0;  // equal times need no sync
+        t_prev = t;
         if (__dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
           if (!synced) break;
           // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
@@ -716,9 +721,6 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
         }
         __syncwarp();
         k++;
-        double tn = __longlong_as_double(0x7ff0000000000000LL);
-        if (k < N) tn = (k < c0 + 32) ? __shfl_sync(FULL, c_t, k - c0) : arr[k];
-        if (!(k < N && tn == t)) synced = 0;  // equal times need no sync
       }
       };
       if (I.balancer == SSB_BAL_SAL) route_loop(BalTag<SSB_BAL_SAL>{});
