@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SSB_ABI_VERSION 1
+#define SSB_ABI_VERSION 2
 
 /* scheduler registry keys, policies.py:279 ("fcfs","nopreempt","trail_plus","larry") */
 enum { SSB_POLICY_FCFS = 0, SSB_POLICY_NOPREEMPT = 1, SSB_POLICY_TRAIL_PLUS = 2, SSB_POLICY_LARRY = 3 };
@@ -92,6 +92,11 @@ typedef struct {
   int32_t run_cap;              /* running-table capacity per server                */
   int32_t est_cost;             /* scheduling hint (larger = start earlier)         */
   int32_t flags;                /* SSB_FLAG_*                                       */
+  /* SAL's token cap: settings.engine.max_tokens_per_batch as run_cluster hands it to
+   * make_balancer (cluster.py:96-104), independent of the engines' own batching cap
+   * (engine.max_tokens_per_batch above), which prebuilt engines may set differently */
+  int32_t route_cap;
+  int32_t _pad1;
 } ssb_instance;
 
 /* Running tables live in shared memory with SSB_SMEM_RUN_CAP entries per
@@ -137,6 +142,27 @@ typedef struct {
                               back as ssb_instance.est_cost to order the next launch)     */
 } ssb_stats;
 
+/* Per-engine counters (one row per server of an instance, server order): the
+ * reference keeps iterations / peak_batch_tokens on each Engine object
+ * (engine.py:165-166,225-226) and its criterion-8 audit reads them per engine
+ * (tests/test_acceptance.py:371-382). Filled by ssb_engine_stats_gather after a
+ * simulation from the per-server state left in the scratch buffer. */
+typedef struct {
+  int64_t iterations;
+  int64_t request_steps;
+  int64_t batch_tokens;
+  int64_t dispatches;
+  int64_t preempts;
+  int64_t parks;
+  int64_t finished;
+  int64_t peak_batch_tokens;
+  uint64_t digest;         /* FNV-1a of this engine's event log (before the instance fold) */
+  int64_t event_count;     /* events this engine produced (> its ring slice = truncated log) */
+  double clock;            /* Engine.clock at the end of the run                            */
+  int32_t status;
+  int32_t _pad;
+} ssb_engine_stats;
+
 /* Optional event log (engine.py:267-274) */
 typedef struct {
   double time;
@@ -163,7 +189,7 @@ typedef struct {
 
 /* Library/ABI identification. ssb_struct_sizes writes sizeof() of
  * ssb_engine_params, ssb_instance, ssb_stats, ssb_event, ssb_summary,
- * ssb_summary_group (in that order) to out[0..5]; returns 6. */
+ * ssb_summary_group, ssb_engine_stats (in that order) to out[0..6]; returns 7. */
 int32_t ssb_abi_version(void);
 const char* ssb_error_string(int32_t code);
 int32_t ssb_struct_sizes(int64_t* out);
@@ -185,6 +211,16 @@ int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* d_inst, int
                      void* d_scratch, size_t scratch_bytes,
                      ssb_event* d_events, int64_t event_cap, int64_t* d_event_count,
                      void* stream /* cudaStream_t */);
+
+/* After ssb_simulate (same stream, same scratch): per-engine counters of every
+ * instance. Row (i, s) = instance i's server s is written to
+ * d_out[d_engine_offset[i] + s] (d_engine_offset: device array of n_inst row
+ * offsets, typically the exclusive prefix sum of n_servers). Replaces reading
+ * engine.iterations / engine.peak_batch_tokens off the engines passed to
+ * run_cluster(..., engines=...) (cluster.py:66-79). */
+int32_t ssb_engine_stats_gather(const ssb_instance* h_inst, const ssb_instance* d_inst, int32_t n_inst,
+                                const void* d_scratch, const int64_t* d_engine_offset,
+                                ssb_engine_stats* d_out, void* stream);
 
 /* One summary group = one summarize(records) call (metrics.py:80-99) over
  * records [record_offset, record_offset+n) whose trace entries are

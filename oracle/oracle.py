@@ -59,7 +59,7 @@ def load():
         ]
         lib.ssb_oracle_rng_integers.restype = None
         lib.ssb_oracle_rng_integers.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
-        sizes = np.zeros(6, dtype=np.int64)
+        sizes = np.zeros(len(_abi.STRUCT_ORDER), dtype=np.int64)
         lib.ssb_oracle_struct_sizes(sizes.ctypes.data)
         for name, got in zip(_abi.STRUCT_ORDER, sizes):
             assert int(got) == _abi.STRUCT_SIZES[name], (name, got)

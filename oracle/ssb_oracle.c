@@ -681,7 +681,7 @@ int ssb_oracle_run(const ssb_instance* inst, ssb_trace trace, ssb_records rec, s
             for (int64_t k = 0; k < n; k++) {
               /* sal_load, balancers.py:103-112 */
               double memory_term = beta * (double)((int64_t)req->prompt - view[k].free_mem);
-              double queue_term = (double)(view[k].queued + req->prompt) / (double)p->max_tokens_per_batch;
+              double queue_term = (double)(view[k].queued + req->prompt) / (double)inst->route_cap; /* settings cap, cluster.py:101 */
               double load = queue_term > memory_term ? queue_term : memory_term;
               if (k == 0 || load < best) { best = load; bi = k; }
             }
@@ -809,5 +809,6 @@ void ssb_oracle_rng_integers(uint64_t state_hi, uint64_t state_lo, uint64_t inc_
 int32_t ssb_oracle_struct_sizes(int64_t* out) {
   out[0] = sizeof(ssb_engine_params); out[1] = sizeof(ssb_instance); out[2] = sizeof(ssb_stats);
   out[3] = sizeof(ssb_event); out[4] = sizeof(ssb_summary); out[5] = sizeof(ssb_summary_group);
-  return 6;
+  out[6] = sizeof(ssb_engine_stats);
+  return 7;
 }

@@ -62,6 +62,8 @@ INSTANCE = np.dtype(
         ("run_cap", "<i4"),
         ("est_cost", "<i4"),
         ("flags", "<i4"),
+        ("route_cap", "<i4"),
+        ("_pad1", "<i4"),
     ],
     align=True,
 )
@@ -80,6 +82,25 @@ STATS = np.dtype(
         ("status", "<i4"),
         ("_pad", "<i4"),
         ("device_cycles", "<i8"),
+    ],
+    align=True,
+)
+
+ENGINE_STATS = np.dtype(
+    [
+        ("iterations", "<i8"),
+        ("request_steps", "<i8"),
+        ("batch_tokens", "<i8"),
+        ("dispatches", "<i8"),
+        ("preempts", "<i8"),
+        ("parks", "<i8"),
+        ("finished", "<i8"),
+        ("peak_batch_tokens", "<i8"),
+        ("digest", "<u8"),
+        ("event_count", "<i8"),
+        ("clock", "<f8"),
+        ("status", "<i4"),
+        ("_pad", "<i4"),
     ],
     align=True,
 )
@@ -130,8 +151,11 @@ STRUCT_SIZES = {
     "ssb_event": EVENT.itemsize,
     "ssb_summary": SUMMARY.itemsize,
     "ssb_summary_group": SUMMARY_GROUP.itemsize,
+    "ssb_engine_stats": ENGINE_STATS.itemsize,
 }
-STRUCT_ORDER = ["ssb_engine_params", "ssb_instance", "ssb_stats", "ssb_event", "ssb_summary", "ssb_summary_group"]
+STRUCT_ORDER = ["ssb_engine_params", "ssb_instance", "ssb_stats", "ssb_event", "ssb_summary", "ssb_summary_group",
+                "ssb_engine_stats"]
+ABI_VERSION = 2
 
 
 class SsbTrace(ctypes.Structure):
@@ -204,6 +228,11 @@ EXPORTS = {
         ],
     ),
     "ssb_struct_sizes": (ctypes.c_int32, [ctypes.c_void_p]),
+    "ssb_engine_stats_gather": (
+        ctypes.c_int32,
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p],
+    ),
 }
 
 _LIB = None
@@ -229,7 +258,7 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ssb_abi_version() != 1:
+    if lib.ssb_abi_version() != ABI_VERSION:
         raise NativeLibraryMissing(f"{p}: ABI version mismatch")
     sizes = np.zeros(len(STRUCT_ORDER), dtype=np.int64)
     lib.ssb_struct_sizes(sizes.ctypes.data)

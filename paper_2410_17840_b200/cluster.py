@@ -71,6 +71,7 @@ class Engine:
         self.peak_batch_tokens = 0
         self.request_steps = 0
         self.batch_tokens = 0
+        self.clock = 0.0
         self.event_log: list[tuple[str, float, int, str]] = []
 
     def run(self, trace, validate: bool = True) -> list[MetricsRecord]:
@@ -103,13 +104,31 @@ class JobResult:
     summary: Summary | None = None
     extras: SummaryExtras | None = None
     events: list = field(default_factory=list)
+    engines: np.ndarray | None = None  # ENGINE_STATS rows, server order
+
+
+def est_status(db, est) -> list[int]:
+    """Each instance's status (the instance's own, else its first failing engine's)."""
+    from . import simulate
+
+    st = db.d_stats.cpu().numpy().view(_abi.STATS)["status"]
+    rows = simulate.engine_rows(db)
+    out = []
+    for i in range(len(db.h_inst)):
+        code = int(st[i])
+        if code == _abi.SSB_OK:
+            bad = est["status"][rows[i]:rows[i + 1]]
+            bad = bad[bad != 0]
+            code = int(bad[0]) if len(bad) else code
+        out.append(code)
+    return out
 
 
 def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, validate: bool = True,
-                  resolved=None) -> list[JobResult]:
-    """Simulate independent instances in one launch. jobs: (settings, trace[, qps_factor[, label]])."""
-    import torch
-
+                  resolved=None, check: bool = False) -> list[JobResult]:
+    """Simulate independent instances in one launch. jobs: (settings, trace[, qps_factor[, label]]).
+    check=True raises the reference's exception (StallError / RuntimeError) for the first
+    instance that did not complete, as a per-instance run_cluster call would."""
     from . import simulate
 
     jobs = list(jobs)
@@ -120,8 +139,7 @@ def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, valida
         for (job, re) in zip(jobs, resolved):
             t = as_trace(job[1])
             f = float(job[2]) if len(job) > 2 else 1.0
-            if validate:
-                I.check_trace(t, re, f)
+            I.check_trace(t, re, f, feasibility=validate)
             recs.append(I.instance_record(job[0], len(t), trace_offset=n_rec, record_offset=n_rec, qps_factor=f,
                                           resolved=re))
             traces.append(t)
@@ -129,13 +147,11 @@ def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, valida
         tr = Trace(np.concatenate([t.arrival for t in traces]), np.concatenate([t.prompt for t in traces]),
                    np.concatenate([t.output for t in traces]))
         batch = I.Batch(tr, np.array(recs, dtype=_abi.INSTANCE), n_rec, [j[3] if len(j) > 3 else None for j in jobs])
-    db = simulate.upload(batch, events=events)
-    simulate.launch(db)
-    torch.cuda.synchronize()
-    if simulate.retry_overflows(db):
-        if events:
-            simulate.launch(db)
-        torch.cuda.synchronize()
+    db, est = simulate.simulate_batch(batch, events=events)
+    rows = simulate.engine_rows(db)
+    if check:
+        for i, st in enumerate(est_status(db, est)):
+            _raise_status(st, f"instance {i} ({batch.labels[i] if i < len(batch.labels) else i})")
     srows = None
     if summaries:
         inst = db.h_inst
@@ -158,7 +174,8 @@ def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, valida
         soa = RecordsSoA(arr, batch.trace.prompt[to:to + n], batch.trace.output[to:to + n],
                          rec.first_token[o:o + n], rec.finish[o:o + n], rec.preempt_count[o:o + n],
                          rec.server[o:o + n], rec.first_dispatch[o:o + n])
-        r = JobResult(batch.labels[i] if i < len(batch.labels) else None, soa, stats[i])
+        r = JobResult(batch.labels[i] if i < len(batch.labels) else None, soa, stats[i],
+                      engines=est[rows[i]:rows[i + 1]].copy())
         if srows is not None and n > 0:
             r.summary, r.extras = _summary_from_row(srows[i])
         if events:
@@ -189,12 +206,37 @@ def run_cluster(settings: ClusterSettings, trace, *, engines: list[Engine] | Non
     _raise_status(int(res.stats["status"]), "run_cluster")
     if engines is not None:
         for s, e in enumerate(engines):
+            row = res.engines[s]
             e._used = True
-            e.iterations = int(res.stats["iterations"]) if n == 1 else e.iterations
-            e.peak_batch_tokens = int(res.stats["peak_batch_tokens"])
-            e.request_steps = int(res.stats["request_steps"]) if n == 1 else e.request_steps
-            e.batch_tokens = int(res.stats["batch_tokens"]) if n == 1 else e.batch_tokens
+            e.iterations = int(row["iterations"])  # engine.py:226
+            e.peak_batch_tokens = int(row["peak_batch_tokens"])  # engine.py:225
+            e.request_steps = int(row["request_steps"])
+            e.batch_tokens = int(row["batch_tokens"])
+            e.clock = float(row["clock"])
             if rec_events:
-                e.event_log = [(_abi.EVENT_NAMES[int(x["code"])], float(x["time"]), int(x["request_id"]), "")
-                               for x in res.events[s]]
+                e.event_log = event_log_with_details(res.events[s])
     return res.records.to_records()
+
+
+def event_log_with_details(ev) -> list[tuple[str, float, int, str]]:
+    """One engine's device event stream as the reference's event_log (engine.py:165,273-274),
+    detail strings included: a dispatch logs its dispatch_seq (the engine's running dispatch
+    count, engine.py:294-298), a preempt / park the request's preempt_count after the
+    increment (engine.py:372-379). Both are counters over this engine's own stream."""
+    names = _abi.EVENT_NAMES
+    out = []
+    seq = 0
+    pcount: dict[int, int] = {}
+    for x in ev:
+        code, rid, t = int(x["code"]), int(x["request_id"]), float(x["time"])
+        if code == 1:  # dispatch
+            detail = f"seq={seq}"
+            seq += 1
+        elif code in (2, 3):  # preempt / park
+            c = pcount.get(rid, 0) + 1
+            pcount[rid] = c
+            detail = f"count={c}"
+        else:
+            detail = ""
+        out.append((names[code], t, rid, detail))
+    return out

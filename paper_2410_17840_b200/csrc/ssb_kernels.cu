@@ -273,6 +273,8 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
     s.device_cycles = clock64() - t0;
     stats[idx] = s;
     if (ev_count) ev_count[idx] = E.st.ev_n;
+    // the engine's final state where a cluster's servers keep theirs (ssb_engine_stats_gather)
+    *(Srv*)(scratch + I.scratch_offset + L.srv) = E.st;
   }
   __syncwarp();
 }
@@ -509,8 +511,10 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
   csync();
 
   const bool est_beta = I.balancer == SSB_BAL_SAL && isnan(I.beta_fixed);
-  const bool cap_pow2 = cfg.cap > 0 && (cfg.cap & (cfg.cap - 1)) == 0;
-  const double inv_cap = cap_pow2 ? __ddiv_rn(1.0, (double)cfg.cap) : 0.0;
+  // SAL's cap is the settings' max_tokens_per_batch (cluster.py:101), not the engines' own
+  const int route_cap = I.route_cap;
+  const bool cap_pow2 = route_cap > 0 && (route_cap & (route_cap - 1)) == 0;
+  const double inv_cap = cap_pow2 ? __ddiv_rn(1.0, (double)route_cap) : 0.0;
   Pcg rng;
   rng.shi = I.pcg_state_hi; rng.slo = I.pcg_state_lo; rng.ihi = I.pcg_inc_hi; rng.ilo = I.pcg_inc_lo;
   rng.has = 0; rng.buf = 0;
@@ -673,7 +677,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           #pragma unroll 1  // n <= 64 in practice: 1-2 trips, no unrolled remainder chain
           for (int q = lane; q < n; q += 32) {
             const double que = cap_pow2 ? __dmul_rn((double)(v_q[q] + pr), inv_cap)
-                                        : __ddiv_rn((double)(v_q[q] + pr), (double)cfg.cap);
+                                        : __ddiv_rn((double)(v_q[q] + pr), (double)route_cap);
             const double mem = __dmul_rn(beta, (double)((long long)pr - v_f[q]));
             const double load = que > mem ? que : mem;
             const unsigned long long k1 = dkey(load), kq = dkey(que);
@@ -829,6 +833,35 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   }
 }
 
+// per-engine counters from the per-server state each simulation leaves in the scratch
+// buffer (k_engines writes its engine's Srv at the end, k_cluster after every advance)
+__global__ void k_engine_stats(const ssb_instance* __restrict__ inst, int n_inst,
+                               const unsigned char* __restrict__ scratch, const int64_t* __restrict__ row0,
+                               ssb_engine_stats* __restrict__ out) {
+  for (int i = blockIdx.x; i < n_inst; i += gridDim.x) {
+    const ssb_instance I = inst[i];
+    const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+    for (int s = threadIdx.x; s < I.n_servers; s += blockDim.x) {
+      const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
+      ssb_engine_stats e;
+      e.iterations = sv->iterations;
+      e.request_steps = sv->rsteps;
+      e.batch_tokens = sv->btokens;
+      e.dispatches = sv->dispatches;
+      e.preempts = sv->preempts;
+      e.parks = sv->parks;
+      e.finished = sv->finished;
+      e.peak_batch_tokens = sv->peak;
+      e.digest = sv->digest;
+      e.event_count = sv->ev_n;
+      e.clock = sv->clock;
+      e.status = sv->status;
+      e._pad = 0;
+      out[row0[i] + s] = e;
+    }
+  }
+}
+
 }  // namespace
 
 // ==========================================================================
@@ -861,7 +894,24 @@ extern "C" int32_t ssb_struct_sizes(int64_t* out) {
   out[3] = sizeof(ssb_event);
   out[4] = sizeof(ssb_summary);
   out[5] = sizeof(ssb_summary_group);
-  return 6;
+  out[6] = sizeof(ssb_engine_stats);
+  return 7;
+}
+
+extern "C" int32_t ssb_engine_stats_gather(const ssb_instance* h_inst, const ssb_instance* d_inst, int32_t n_inst,
+                                           const void* d_scratch, const int64_t* d_engine_offset,
+                                           ssb_engine_stats* d_out, void* stream_) {
+  if (n_inst <= 0) return SSB_OK;
+  if (!h_inst || !d_inst || !d_scratch || !d_engine_offset || !d_out) return SSB_E_ARG;
+  int max_servers = 1;
+  for (int i = 0; i < n_inst; ++i) {
+    if (h_inst[i].n_servers < 1) return SSB_E_ARG;
+    max_servers = std::max(max_servers, h_inst[i].n_servers);
+  }
+  const int threads = std::min(256, (max_servers + 31) / 32 * 32);
+  k_engine_stats<<<(unsigned)std::min(n_inst, 4096), threads, 0, (cudaStream_t)stream_>>>(
+      d_inst, n_inst, (const unsigned char*)d_scratch, d_engine_offset, d_out);
+  return cudaGetLastError() == cudaSuccess ? SSB_OK : SSB_E_CUDA;
 }
 
 extern "C" size_t ssb_prepare(ssb_instance* h, int32_t n_inst) {

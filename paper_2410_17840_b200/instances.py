@@ -67,12 +67,26 @@ def engine_params_record(re: ResolvedEngine) -> np.void:
     return rec
 
 
-def check_trace(trace: Trace, re: ResolvedEngine, qps_factor: float = 1.0) -> None:
-    """run_cluster's validation: sorted arrivals then feasibility (cluster.py:80-92)."""
-    arr = trace.arrival if qps_factor == 1.0 else trace.arrival / qps_factor
+def check_qps_factor(qps_factor: float) -> float:
+    """scale_qps's argument check (workload.py:187-194)."""
+    f = float(qps_factor)
+    if not f > 0 or not np.isfinite(f):
+        raise ValueError(f"factor must be > 0, got {qps_factor}")
+    return f
+
+
+def check_trace(trace: Trace, re: ResolvedEngine, qps_factor: float = 1.0, *, feasibility: bool = True) -> None:
+    """run_cluster's validation (cluster.py:80-92): the TraceEntry field checks
+    (workload.py:50-56; a Trace built from arrays never ran them), sorted arrivals —
+    both always, as the reference's run()/run_cluster do — then, unless
+    ``feasibility`` is False (the reference's validate=False), check_feasible."""
+    trace.validate()
+    f = check_qps_factor(qps_factor)
+    arr = trace.arrival if f == 1.0 else trace.arrival / f
     if len(arr) > 1 and np.any(arr[1:] < arr[:-1]):
         raise ValueError("trace arrivals must be sorted")
-    re.policy.check_feasible_many(trace.prompt, trace.output, re.block_size, re.pool_blocks, re.limits)
+    if feasibility:
+        re.policy.check_feasible_many(trace.prompt, trace.output, re.block_size, re.pool_blocks, re.limits)
 
 
 def instance_record(
@@ -95,6 +109,7 @@ def instance_record(
     if bs.name == "sal":
         BetaEstimator(prior=bs.beta_prior)  # balancers.py:74-75
     re = resolved or resolve_engine(settings.engine)
+    qps_factor = check_qps_factor(qps_factor)
     rec = np.zeros((), dtype=_abi.INSTANCE)
     rec["engine"] = engine_params_record(re)
     rec["n_servers"] = settings.n_servers
@@ -108,6 +123,8 @@ def instance_record(
     rec["trace_offset"] = trace_offset
     rec["record_offset"] = record_offset
     rec["n_requests"] = n_requests
+    # SAL's cap comes from the settings, not from the (possibly prebuilt) engines (cluster.py:96-104)
+    rec["route_cap"] = int(settings.engine.max_tokens_per_batch)
     return rec
 
 
@@ -127,6 +144,7 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
     the kernel's trace read)."""
     traces: list[Trace] = []
     trace_index: dict[int, int] = {}
+    keep_alive: list = []  # every keyed trace object lives until the loop ends, so no id() is reused
     trace_offs: list[int] = []
     recs = []
     labels = []
@@ -137,6 +155,7 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
         label = job[3] if len(job) > 3 else None
         t = as_trace(trace)
         key = id(trace)
+        keep_alive.append(trace)
         if key not in trace_index:
             trace_index[key] = len(traces)
             traces.append(t)
@@ -144,8 +163,7 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
             n_trace += len(t)
         toff = trace_offs[trace_index[key]]
         re = resolve_engine(settings.engine)
-        if validate:
-            check_trace(t, re, factor)
+        check_trace(t, re, factor, feasibility=validate)
         recs.append(
             instance_record(
                 settings, len(t), trace_offset=toff, record_offset=n_records, qps_factor=factor, resolved=re

@@ -218,7 +218,9 @@ def capacity_sweep(cluster_settings, trace, factors) -> list[tuple[float, Summar
     from .cluster import simulate_jobs
 
     jobs = [(cluster_settings, trace, float(f)) for f in factors]
-    res = simulate_jobs(jobs, summaries=True)
+    # per factor the reference's run_cluster raises (StallError / RuntimeError) instead of
+    # summarising an incomplete run; scale_qps raises ValueError for factor <= 0 (make_batch)
+    res = simulate_jobs(jobs, summaries=True, check=True)
     return [(float(f), r.summary) for f, r in zip(factors, res)]
 
 

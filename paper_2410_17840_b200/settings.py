@@ -80,17 +80,21 @@ _COST_DEFAULTS = {  # costmodel.py:62-75
 
 
 def default_params(profile_name: str, hardware: str, **overrides: float) -> CostParams:
-    """Cost parameters for a (profile, hardware) pair (costmodel.py:78-94)."""
-    key = (profile_name, hardware)
-    if key in _COST_DEFAULTS:
-        base = _COST_DEFAULTS[key]
-        return replace(base, **overrides) if overrides else base
-    required = {"mem_base_s", "mem_per_kv_token_s", "compute_per_token_s", "overhead_s"}
-    if set(overrides) == required:
-        return CostParams(**overrides)
-    raise KeyError(
-        f"no default cost parameters for {profile_name!r} on {hardware!r}; known pairs: {sorted(_COST_DEFAULTS)}"
-    )
+    """Cost parameters for a (profile, hardware) pair (costmodel.py:78-94): the known
+    pairs' defaults with per-field overrides; an unknown pair needs all four fields."""
+    fields_ = ("mem_base_s", "mem_per_kv_token_s", "compute_per_token_s", "overhead_s")
+    base = _COST_DEFAULTS.get((profile_name, hardware))
+    if base is None and set(overrides) != set(fields_):
+        raise KeyError(
+            f"no default cost parameters for {profile_name!r} on {hardware!r}; known pairs: {sorted(_COST_DEFAULTS)}"
+        )
+    if base is None or overrides:
+        vals = {f: overrides.get(f, getattr(base, f) if base is not None else None) for f in fields_}
+        unknown = set(overrides) - set(fields_)
+        if unknown:
+            raise TypeError(f"unknown cost parameter(s): {sorted(unknown)}")
+        return CostParams(**vals)
+    return base
 
 
 @dataclass
@@ -132,58 +136,20 @@ class ClusterSettings:
 
 
 class KvBlockPool:
-    """Host-side KV block accounting object (kvmem.py:74-154), kept for API parity
-    (Engine(pool, ...) construction, unit checks). The simulation itself keeps
-    the pool on the device as a free-block counter plus per-request
-    prompt+generated token counts (csrc/ssb_engine.cuh)."""
+    """Pool descriptor for ``Engine(KvBlockPool(total_blocks, block_size), ...)``
+    construction (kvmem.py:74-104 constructor and validation). The block
+    accounting itself (try_allocate / try_grow / free, kvmem.py:106-154) runs on
+    the device as one free-block counter per engine plus each running request's
+    prompt+generated token count (csrc/ssb_engine.cuh); there is no host copy."""
 
     def __init__(self, total_blocks: int, block_size: int = DEFAULT_BLOCK_SIZE):
         if total_blocks < 0:
             raise ValueError(f"total_blocks must be >= 0, got {total_blocks}")
         if block_size < 1:
             raise ValueError(f"block_size must be >= 1, got {block_size}")
-        self.total_blocks = total_blocks
-        self.block_size = block_size
-        self.free_blocks = total_blocks
-        self._tokens: dict[int, int] = {}
+        self.total_blocks = int(total_blocks)
+        self.block_size = int(block_size)
+        self.free_blocks = self.total_blocks  # a fresh pool; engines are run once (engine.py:238-239)
 
-    def allocated_tokens(self, request_id: int) -> int:
-        return self._tokens[request_id]
-
-    def allocated_blocks(self, request_id: int) -> int:
-        return blocks_needed(self._tokens[request_id], self.block_size)
-
-    def try_allocate(self, request_id: int, tokens: int) -> bool:
-        if request_id in self._tokens:
-            raise ValueError(f"request {request_id} already holds an allocation")
-        need = blocks_needed(tokens, self.block_size)
-        if need > self.free_blocks:
-            return False
-        self._tokens[request_id] = tokens
-        self.free_blocks -= need
-        return True
-
-    def try_grow(self, request_id: int, new_total_tokens: int) -> bool:
-        if request_id not in self._tokens:
-            raise KeyError(f"request {request_id} holds no allocation")
-        current = self._tokens[request_id]
-        if new_total_tokens < current:
-            raise ValueError(f"allocation for request {request_id} cannot shrink")
-        extra = blocks_needed(new_total_tokens, self.block_size) - blocks_needed(current, self.block_size)
-        if extra > self.free_blocks:
-            return False
-        self._tokens[request_id] = new_total_tokens
-        self.free_blocks -= extra
-        return True
-
-    def free(self, request_id: int) -> int:
-        if request_id not in self._tokens:
-            raise KeyError(f"request {request_id} holds no allocation")
-        released = self.allocated_blocks(request_id)
-        del self._tokens[request_id]
-        self.free_blocks += released
-        return released
-
-    def conserved(self) -> bool:
-        held = sum(blocks_needed(t, self.block_size) for t in self._tokens.values())
-        return self.free_blocks + held == self.total_blocks and self.free_blocks >= 0
+    def __repr__(self) -> str:
+        return f"KvBlockPool(total_blocks={self.total_blocks}, block_size={self.block_size})"

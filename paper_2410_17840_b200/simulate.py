@@ -85,6 +85,8 @@ class DeviceBatch:
     d_events: object = None
     d_evcount: object = None
     event_cap: int = 0
+    d_engine_offset: object = None  # row of (instance i, server 0) in the per-engine stats
+    n_engines: int = 0
 
     def trace_c(self) -> _abi.SsbTrace:
         return _abi.SsbTrace(self.d_arrival.data_ptr(), self.d_prompt.data_ptr(), self.d_output.data_ptr())
@@ -119,13 +121,68 @@ def upload(batch: Batch, *, device=None, events: bool = False, event_cap: int | 
         d_scratch=torch.empty(max(scratch_bytes, 256), dtype=torch.uint8, device=device),
         scratch_bytes=scratch_bytes,
     )
+    ns = h_inst["n_servers"].astype(np.int64) if len(h_inst) else np.zeros(0, np.int64)
+    db.n_engines = int(ns.sum())
+    db.d_engine_offset = _np_to_dev(torch, np.concatenate([[0], np.cumsum(ns)[:-1]]).astype(np.int64)
+                                    if len(ns) else np.zeros(1, np.int64), device)
     if events:
+        # first guess: 4 events per request (enqueue, dispatch, first_token, finish) + 2 per
+        # preemption; an engine that outgrows its slice is detected after the run
+        # (ssb_engine_stats.event_count) and the batch re-runs with a larger ring
         cap = event_cap or int(max(1, max((int(i["n_requests"]) for i in h_inst), default=1)) * 12 + 64)
         cap = cap * int(max((int(i["n_servers"]) for i in h_inst), default=1))
-        db.event_cap = cap
-        db.d_events = torch.empty(len(h_inst) * cap * _abi.EVENT.itemsize, dtype=torch.uint8, device=device)
-        db.d_evcount = torch.zeros(len(h_inst), dtype=torch.int64, device=device)
+        alloc_events(db, cap)
     return db
+
+
+def alloc_events(db: DeviceBatch, cap: int) -> None:
+    """(Re)allocate the per-instance event rings: `cap` entries per instance, split evenly
+    between the instance's servers by the kernels."""
+    torch = _torch()
+    device = db.d_inst.device
+    db.event_cap = int(cap)
+    db.d_events = torch.empty(len(db.h_inst) * db.event_cap * _abi.EVENT.itemsize, dtype=torch.uint8, device=device)
+    db.d_evcount = torch.zeros(len(db.h_inst), dtype=torch.int64, device=device)
+
+
+def engine_stats(db: DeviceBatch, stream=None) -> np.ndarray:
+    """Per-engine counters of the last simulation (ENGINE_STATS rows; instance i's server
+    s at row offsets[i] + s). Synchronises."""
+    torch = _torch()
+    lib = _abi.load_library()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    out = torch.empty(max(db.n_engines, 1) * _abi.ENGINE_STATS.itemsize, dtype=torch.uint8, device=db.d_inst.device)
+    rc = lib.ssb_engine_stats_gather(db.h_inst.ctypes.data, db.d_inst.data_ptr(), len(db.h_inst),
+                                     db.d_scratch.data_ptr(), db.d_engine_offset.data_ptr(), out.data_ptr(),
+                                     ctypes.c_void_p(stream.cuda_stream))
+    if rc != 0:
+        raise SimulationError(f"ssb_engine_stats_gather: {lib.ssb_error_string(rc).decode()} ({rc})")
+    return out.cpu().numpy().view(_abi.ENGINE_STATS)[: db.n_engines].copy()
+
+
+def engine_rows(db: DeviceBatch) -> np.ndarray:
+    """Row offset of each instance's first engine in engine_stats()."""
+    ns = db.h_inst["n_servers"].astype(np.int64)
+    return np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
+
+
+def event_overflow_cap(db: DeviceBatch, est: np.ndarray) -> int:
+    """0 if every engine's events fit its ring slice, else the per-instance capacity that
+    makes the largest engine log fit (the kernels never drop an event silently: they keep
+    counting past the slice, and this is where the count is read)."""
+    if db.d_events is None or len(est) == 0:
+        return 0
+    rows = engine_rows(db)
+    need = 0
+    over = False
+    for i, inst in enumerate(db.h_inst):
+        ns = int(inst["n_servers"])
+        cnt = est["event_count"][rows[i]:rows[i + 1]]
+        m = int(cnt.max()) if len(cnt) else 0
+        over |= m > db.event_cap // ns
+        need = max(need, m * ns)
+    return need + 64 * int(db.h_inst["n_servers"].max()) if over else 0
 
 
 def launch(db: DeviceBatch, stream=None) -> None:
@@ -207,8 +264,10 @@ def retry_overflows(db: DeviceBatch, stats_host: np.ndarray | None = None) -> in
     return len(redo)
 
 
-def run_batch(batch: Batch, *, events: bool = False, event_cap: int | None = None, check: bool = False):
-    """Upload, simulate, download. Returns (records, stats[, events])."""
+def simulate_batch(batch: Batch, *, events: bool = False, event_cap: int | None = None):
+    """Upload, simulate (re-running shared-table overflows with global tables, and the
+    whole batch with larger event rings if any engine's log outgrew its slice).
+    Returns (db, per-engine stats)."""
     torch = _torch()
     db = upload(batch, events=events, event_cap=event_cap)
     launch(db)
@@ -217,7 +276,25 @@ def run_batch(batch: Batch, *, events: bool = False, event_cap: int | None = Non
         if events:  # event slices are indexed by instance: re-run the whole batch
             launch(db)
         torch.cuda.synchronize()
+    est = engine_stats(db)
+    while events:
+        cap = event_overflow_cap(db, est)
+        if not cap:
+            break
+        alloc_events(db, cap)
+        launch(db)
+        torch.cuda.synchronize()
+        est = engine_stats(db)
+    return db, est
+
+
+def run_batch(batch: Batch, *, events: bool = False, event_cap: int | None = None, check: bool = False,
+              with_engines: bool = False):
+    """Upload, simulate, download. Returns (records, stats[, events][, engine stats])."""
+    db, est = simulate_batch(batch, events=events, event_cap=event_cap)
     out = download(db)
+    if with_engines:
+        out = (*out, est)
     if check:
         bad = np.flatnonzero(out[1]["status"] != 0)
         if len(bad):

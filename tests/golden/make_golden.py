@@ -14,7 +14,8 @@ cluster.py:65-79) and records:
     folded in server order (tests/golden_util.py);
   * a sha256 of the records (first_token, finish, preempt_count, server);
   * summarize() (metrics.py:80-99) of the records;
-  * for the small groups, the full records and event streams.
+  * per engine: iterations, request-steps, batch tokens, peak batch tokens;
+  * for the small groups, the full records, event streams and event_lines().
 Output: tests/golden/<group>.json (committed). Nothing at test or bench time
 reads /root/reference.
 """
@@ -102,7 +103,7 @@ def run_scenario(sc, full: bool):
     else:
         settings = ClusterSettings(
             n_servers=c["n_servers"],
-            engine=EngineSettings(max_tokens_per_batch=e["cap"]),
+            engine=EngineSettings(max_tokens_per_batch=c.get("route_cap", e["cap"])),
             balancer=BalancerSettings(name=c["balancer"], poll_interval_s=c["poll_interval_s"],
                                       beta_prior=c["beta_prior"], beta_fixed=c["beta_fixed"]),
             seed=c["seed"],
@@ -133,10 +134,15 @@ def run_scenario(sc, full: bool):
                                    [r.preempt_count for r in records], [r.server for r in records]),
         "summary": ref_metrics.summarize(records).to_dict() if records else None,
         "ref_wall_s": wall,
+        # per engine (server order): iterations (engine.py:226), request-steps, batch tokens,
+        # peak_batch_tokens (engine.py:225) — the criterion-8 audit is per engine (test_acceptance.py:371-382)
+        "per_engine": [[eng.iterations, getattr(eng, "_g_rsteps", 0), getattr(eng, "_g_btok", 0),
+                        eng.peak_batch_tokens] for eng in engines],
     }
     if full:
         out["records"] = [[r.first_token_time, r.finish_time, r.preempt_count, r.server] for r in records]
         out["events"] = [[[code, rid, t] for code, rid, t in ev] for ev in ev_lists]
+        out["event_lines"] = [eng.event_lines() for eng in engines]  # engine.py:267-269, incl. seq=/count=
     return out
 
 

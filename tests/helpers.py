@@ -49,7 +49,8 @@ def scenario_trace(sc) -> Trace:
 def scenario_settings(sc) -> tuple[ClusterSettings, I.ResolvedEngine]:
     e, c = sc["engine"], sc["cluster"]
     es = EngineSettings(policy=e["policy"], alpha=e["alpha"], c=e["c"], max_output=e["max_output"],
-                        pool_blocks=e["pool_blocks"], block_size=e["block_size"], max_tokens_per_batch=e["cap"],
+                        pool_blocks=e["pool_blocks"], block_size=e["block_size"],
+                        max_tokens_per_batch=c.get("route_cap", e["cap"]),
                         max_running=e["max_running"],
                         cost=dict(zip(["mem_base_s", "mem_per_kv_token_s", "compute_per_token_s", "overhead_s"],
                                       e["cost"])))
@@ -84,8 +85,12 @@ def scenario_batch(scs) -> I.Batch:
     return I.Batch(tr, np.array(recs, dtype=I._abi.INSTANCE), n_rec, [sc["name"] for sc in scs])
 
 
-def compare_instance(sc, golden, batch, i, rec, stats, *, check_summary=None) -> list[str]:
-    """Return a list of mismatch descriptions (empty = bit-exact parity)."""
+PER_ENGINE_FIELDS = ("iterations", "request_steps", "batch_tokens", "peak_batch_tokens")
+
+
+def compare_instance(sc, golden, batch, i, rec, stats, *, check_summary=None, engines=None) -> list[str]:
+    """Return a list of mismatch descriptions (empty = bit-exact parity). engines: the
+    instance's ENGINE_STATS rows, compared with the reference's per-engine counters."""
     g = golden[sc["name"]]
     bad = []
     st = stats[i]
@@ -107,6 +112,10 @@ def compare_instance(sc, golden, batch, i, rec, stats, *, check_summary=None) ->
             bad.append(f"{k}: got {int(st[k])} want {g[k]}")
     if "%016x" % int(st["digest"]) != g["digest"]:
         bad.append("event digest differs")
+    if engines is not None and "per_engine" in g:
+        got = [[int(r[k]) for k in PER_ENGINE_FIELDS] for r in engines]
+        if got != g["per_engine"]:
+            bad.append(f"per-engine counters differ: got {got[:3]} want {g['per_engine'][:3]}")
     sha = records_sha(rec.first_token[o:o + n], rec.finish[o:o + n], rec.preempt_count[o:o + n],
                       rec.server[o:o + n])
     if sha != g["records_sha"]:

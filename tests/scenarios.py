@@ -235,18 +235,20 @@ def cluster_unit_scenarios():
 
 
 def fuzz_cluster_scenarios(n=96, seed=31337, block_sizes=(4, 16), prefix="fuzzcl", caps=(32, 256, 1024),
-                           betas=(1.0, 2.0, 6.5), bals=("rr", "random", "p2c", "sal")):
+                           betas=(1.0, 2.0, 6.5), bals=("rr", "random", "p2c", "sal"), servers=None,
+                           pols=("fcfs", "nopreempt", "trail_plus", "larry"), nreq_range=(5, 150)):
     """Randomised multi-replica instances: every balancer x policy, tight pools,
-    poll intervals from 1 ms to inf, fixed and estimated beta, equal-time bursts."""
+    poll intervals from 1 ms to inf, fixed and estimated beta, equal-time bursts.
+    servers: replica counts to cycle through (default: uniform in 2..8)."""
     rng = np.random.default_rng(seed)
     out = []
     bals = list(bals)
-    pols = ["fcfs", "nopreempt", "trail_plus", "larry"]
+    pols = list(pols)
     for i in range(n):
         b = bals[i % len(bals)]
-        pol = pols[(i // len(bals)) % 4]
-        ns = int(rng.integers(2, 9))
-        nreq = int(rng.integers(5, 150))
+        pol = pols[(i // len(bals)) % len(pols)]
+        ns = int(rng.integers(2, 9)) if servers is None else int(servers[(i // (len(bals) * len(pols))) % len(servers)])
+        nreq = int(rng.integers(*nreq_range))
         if rng.random() < 0.3:
             arrivals = np.sort(np.round(rng.uniform(0, 1.0, nreq), 1))
         else:
@@ -318,6 +320,24 @@ def config_scenarios(full=True):
     return out
 
 
+def prebuilt_scenarios():
+    """run_cluster(settings, trace, engines=[...]) with prebuilt engines whose batching cap
+    differs from settings.engine.max_tokens_per_batch: SAL's queue term divides by the
+    settings' cap (cluster.py:96-104), each engine batches with its own (engine.py:300-323)."""
+    out = []
+    for i, (eng_cap, route_cap) in enumerate([(256, 1024), (1024, 256), (512, 100), (96, 4096)]):
+        for beta_fixed in (None, 2.0):
+            for ns in (3, 12):
+                out.append(scen(f"prebuilt_{eng_cap}_{route_cap}_{beta_fixed}_{ns}",
+                                engine("larry" if i % 2 else "fcfs", pool_blocks=900, cost=COST_A100_8B, cap=eng_cap),
+                                synth(duration_s=20.0, mean_qps=25.0, burstiness=2.0, prompt_dist=CHAT_PROMPT,
+                                      output_dist=CHAT_OUTPUT, seed=40 + i),
+                                mode="cluster",
+                                clus=dict(cluster(ns, "sal", poll_interval_s=0.05, beta_fixed=beta_fixed, seed=i),
+                                          route_cap=route_cap)))
+    return out
+
+
 GROUPS = {
     "engine_unit": engine_unit_scenarios,
     "c6": c6_scenarios,
@@ -333,6 +353,12 @@ GROUPS = {
     + fuzz_cluster_scenarios(24, seed=4243, block_sizes=(3, 10, 24), prefix="oddcl"),
     # sal / p2c routing off the integer-key fast path: token caps that are not powers of two
     # (the queue term is a true division) beside power-of-two ones, fixed and estimated beta
+    # multi-CTA thread-block clusters: 9..64 replicas (2..8 CTAs, one warp per replica) x every
+    # policy x every balancer, and 65..96 replicas (several replicas per warp, global tables)
+    "fuzz_multicta": lambda: fuzz_cluster_scenarios(80, seed=6464, prefix="mcta", servers=(9, 16, 24, 33, 64),
+                                                    nreq_range=(60, 700))
+    + fuzz_cluster_scenarios(32, seed=6565, prefix="mcta_big", servers=(65, 96), nreq_range=(100, 900)),
+    "prebuilt": prebuilt_scenarios,
     "fuzz_route": lambda: fuzz_cluster_scenarios(48, seed=5151, block_sizes=(4, 16), prefix="route",
                                                  caps=(48, 100, 1000, 1024), betas=(1.0, 1.25, 9.0),
                                                  bals=("sal", "sal", "p2c")),

@@ -93,3 +93,32 @@ def test_c1_and_c2_full_size_match_oracle():
         batch, rec, st = _run(jobs)
         _properties(batch, rec, st)
         _check_vs_oracle(batch, rec, st)
+
+
+@pytest.mark.slow
+def test_c3_full_size_matches_oracle_golden():
+    """BASELINE config 3 at its stated size (~1M requests per policy, fcfs and trail_plus
+    c=0.5, pool 1,536 blocks): every counter, the decision digest and a sha256 of every
+    record column equal tests/golden/c3_full.json, which the oracle wrote in the build
+    container (tools/make_c3_golden.py; ~1 h of CPU, the oracle itself being pinned to
+    the reference's own outputs by test_oracle_golden.py)."""
+    import hashlib
+    import json
+    from pathlib import Path
+
+    from paper_2410_17840_b200 import configs as C
+
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "c3_full.json").read_text())
+    batch, rec, st = _run(C.c3_jobs(g["duration_s"]))
+    h = hashlib.sha256()
+    for a in (batch.trace.arrival, batch.trace.prompt, batch.trace.output):
+        h.update(np.ascontiguousarray(a).tobytes())
+    assert h.hexdigest() == g["trace_sha256"], "trace synthesis changed"
+    _properties(batch, rec, st)
+    for i, want in enumerate(g["instances"]):
+        for k in KEYS:
+            assert int(st[i][k]) == want[k], (want["label"], k, int(st[i][k]), want[k])
+        o, n = int(batch.instances[i]["record_offset"]), int(batch.instances[i]["n_requests"])
+        for col, sha in want["records_sha256"].items():
+            got = hashlib.sha256(np.ascontiguousarray(getattr(rec, col)[o:o + n]).tobytes()).hexdigest()
+            assert got == sha, (want["label"], col)

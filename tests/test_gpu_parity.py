@@ -11,7 +11,8 @@ from helpers import compare_instance, load_golden, scenario_batch
 
 pytestmark = pytest.mark.gpu
 
-GROUPS = ["engine_unit", "cluster_unit", "c2", "c3", "c6", "fuzz_engine", "fuzz_cluster", "fuzz_odd_blocks", "fuzz_route"]
+GROUPS = ["engine_unit", "cluster_unit", "c2", "c3", "c6", "fuzz_engine", "fuzz_cluster", "fuzz_odd_blocks", "fuzz_route",
+          "fuzz_multicta", "prebuilt"]
 
 
 def _sim():
@@ -25,10 +26,11 @@ def test_gpu_matches_reference(group):
     golden = load_golden(group)
     scs = S.GROUPS[group]()
     batch = scenario_batch(scs)
-    rec, stats = _sim().run_batch(batch)
+    rec, stats, est = _sim().run_batch(batch, with_engines=True)
+    rows = np.concatenate([[0], np.cumsum(batch.instances["n_servers"])])
     failures = {}
     for i, sc in enumerate(scs):
-        bad = compare_instance(sc, golden, batch, i, rec, stats)
+        bad = compare_instance(sc, golden, batch, i, rec, stats, engines=est[rows[i]:rows[i + 1]])
         if bad:
             failures[sc["name"]] = bad
     assert not failures, f"{len(failures)} mismatches: " + repr(dict(list(failures.items())[:4]))
@@ -50,6 +52,55 @@ def test_gpu_cluster_event_streams_match_reference():
     scs = [s for s in S.cluster_unit_scenarios() if "events" in golden[s["name"]]]
     batch = scenario_batch(scs)
     rec, stats, evs = _sim().run_batch(batch, events=True)
+    for sc, ev in zip(scs, evs):
+        for s, want_s in enumerate(golden[sc["name"]]["events"]):
+            got = [(int(e["code"]), int(e["request_id"]), float(e["time"])) for e in ev[s]]
+            assert got == [tuple(e) for e in want_s], (sc["name"], s)
+
+
+def _engines_for(sc):
+    """Prebuilt engines for a scenario, recording their event logs (cluster.py:66-79)."""
+    import paper_2410_17840_b200 as P
+    from helpers import scenario_settings
+
+    cs, re = scenario_settings(sc)
+    n = sc["cluster"]["n_servers"] if sc["mode"] == "cluster" else 1
+    return cs, [P.Engine(P.KvBlockPool(re.pool_blocks, re.block_size), re.policy, re.cost,
+                         max_tokens_per_batch=re.limits.max_tokens_per_batch, max_running=re.limits.max_running,
+                         max_context=re.limits.max_context, record_events=True) for _ in range(n)]
+
+
+@pytest.mark.parametrize("group", ["engine_unit", "cluster_unit"])
+def test_gpu_event_lines_byte_identical(group):
+    """Engine.event_lines() (engine.py:267-269) through the public run_cluster(engines=...) /
+    Engine.run API: event, repr(time), request id and the seq= / count= details."""
+    import paper_2410_17840_b200 as P
+    from helpers import scenario_trace
+
+    golden = load_golden(group)
+    scs = [s for s in S.GROUPS[group]() if "event_lines" in golden[s["name"]]]
+    assert scs
+    for sc in scs:
+        cs, engines = _engines_for(sc)
+        tr = scenario_trace(sc)
+        if sc["mode"] == "engine":
+            engines[0].run(tr)
+        else:
+            P.run_cluster(cs, tr, engines=engines)
+        for s, e in enumerate(engines):
+            assert e.event_lines() == golden[sc["name"]]["event_lines"][s], (sc["name"], s)
+        want = golden[sc["name"]]["per_engine"]
+        assert [[e.iterations, e.request_steps, e.batch_tokens, e.peak_batch_tokens] for e in engines] == want
+
+
+def test_gpu_event_ring_overflow_reruns():
+    """A ring far too small for the preemption-heavy logs: the engines keep counting past
+    their slice, the host reads the counts and re-runs with a larger ring — the streams
+    still equal the reference's, never truncated."""
+    golden = load_golden("cluster_unit")
+    scs = [s for s in S.cluster_unit_scenarios() if "events" in golden[s["name"]]]
+    batch = scenario_batch(scs)
+    rec, stats, evs = _sim().run_batch(batch, events=True, event_cap=8)
     for sc, ev in zip(scs, evs):
         for s, want_s in enumerate(golden[sc["name"]]["events"]):
             got = [(int(e["code"]), int(e["request_id"]), float(e["time"])) for e in ev[s]]

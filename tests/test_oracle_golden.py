@@ -8,7 +8,8 @@ import scenarios as S
 from helpers import compare_instance, load_golden, scenario_batch
 from oracle import oracle as O
 
-GROUPS_FAST = ["engine_unit", "cluster_unit", "c2", "c3", "fuzz_engine", "fuzz_cluster", "c6", "fuzz_odd_blocks", "fuzz_route"]
+GROUPS_FAST = ["engine_unit", "cluster_unit", "c2", "c3", "fuzz_engine", "fuzz_cluster", "c6", "fuzz_odd_blocks", "fuzz_route",
+               "fuzz_multicta", "prebuilt"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -65,3 +66,22 @@ def test_oracle_summary_matches_reference():
                         rec.preempt_count[o:o + n])
         for k, v in golden[sc["name"]]["summary"].items():
             assert s[k] == v, (sc["name"], k)
+
+
+@pytest.mark.parametrize("group", ["engine_unit", "cluster_unit"])
+def test_event_details_rebuilt_from_device_streams(group):
+    """The host rebuilds the reference's detail strings (dispatch seq=, preempt/park count=,
+    engine.py:294-298,372-379) from (code, id, time) streams like the device ring's: the
+    oracle's streams, split per server, must give event_lines() byte for byte."""
+    from paper_2410_17840_b200.cluster import Engine, event_log_with_details
+
+    golden = load_golden(group)
+    scs = [s for s in S.GROUPS[group]() if "event_lines" in golden[s["name"]]]
+    batch = scenario_batch(scs)
+    _, _, evs = O.run_batch(batch, events=True)
+    for sc, ev in zip(scs, evs):
+        want = golden[sc["name"]]["event_lines"]
+        for s in range(len(want)):
+            e = Engine.__new__(Engine)
+            e.event_log = event_log_with_details(ev[ev["server"] == s])
+            assert e.event_lines() == want[s], (sc["name"], s)
