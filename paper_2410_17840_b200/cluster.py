@@ -65,6 +65,7 @@ class Engine:
                                                                         max_context))
         self.record_events = record_events
         self.policy = policy
+        self.cost = cost
         self.limits = self.resolved.limits
         self._used = False
         self.iterations = 0
