@@ -1,22 +1,39 @@
 #!/usr/bin/env python
-"""Benchmark: simulated request-steps/s of the BASELINE config-4 sweep.
+"""Benchmark: simulated request-steps/s of the BASELINE config-4 sweep (+ a C5 figure).
 
-One *step* = one full policy/config sweep on each GPU: 4 policies x 4 KV
-pools x 16 arrival-rate factors x 16 seeds = 4,096 independent
-single-replica instances (~1.8k requests each, ~7.4M requests, ~1.6e9
-request-steps), simulated by the sm_100a kernels and summarised on the
-device (exact nearest-rank percentiles per instance). Weak scaling: rank r
-simulates seeds 16r..16r+15; for N>1 the per-instance summaries are
-all-gathered (NCCL) inside the step.
+One *step* = one full policy/config sweep: 4 policies x 4 KV pools x 16
+arrival-rate factors x 16 seeds = 4,096 independent single-replica instances
+(~1.8k requests each, ~7.4M requests, ~1.56e9 request-steps), simulated by the
+sm_100a kernels and summarised on the device (exact nearest-rank percentiles per
+instance); for N>1 the per-instance summaries are all-gathered (NCCL) inside the
+step.
 
-  value : request-steps/s, inputs resident in HBM, kernels only
-  e2e   : same metric through SweepRunner.run(): pinned host -> device copy of
-          the trace + instance table, simulate, summarise, device -> host copy
-          of the per-instance stats + summaries, every step
-  --impl reference : the CPU oracle (C restatement of the reference
-          algorithm, oracle/ssb_oracle.c) on all host cores, one seed's sweep
-          (256 instances) per step.
+  --scaling weak   (default) every GPU runs its own 4,096-instance sweep (rank r:
+                   seeds 16r..16r+15)
+  --scaling strong the one 4,096-instance sweep split across the N GPUs
+                   (shard.strong_shard: longest-processing-time by estimated cost)
+
+  value : request-steps/s, inputs resident in HBM, kernels only, the schedule a
+          first run of the sweep gets (host cost estimates, simulate.estimate_cost)
+  warm_schedule : the same after one untimed pass fed back each instance's measured
+          cost (placement only: identical work and results)
+  e2e   : the public API end to end, every step: SweepRunner(jobs) (validation,
+          feasibility, planning, pinned host -> device copies) + run (simulate +
+          summarise) + device -> host copy of the per-instance stats and summaries
+  c5    : BASELINE config 5 shape (64-replica clusters, larry, sal and rr) at
+          16 clusters per GPU on a prefix of the trace, next to the oracle on the
+          same 16 clusters (bit-exact check)
+  --impl reference : the CPU oracle (C restatement of the reference algorithm,
+          oracle/ssb_oracle.c) on all host cores; each step one quarter of the
+          sweep (a fixed random partition, longest-first), the four quarters in
+          rotation, plus one full-sweep pass reported beside it
+  --dry-cpu : the N-rank plumbing (launcher, sharding, barriers, max-over-ranks,
+          all-gather, the JSON line) on gloo with the oracle standing in for the
+          kernels on a small sweep -- a CPU test of the N>1 path, never a bench value
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                       [--scaling weak|strong] [--dry-cpu]
+With --gpus N > 1 and no torchrun environment, bench.py launches itself under
+torch.distributed.run with N ranks (127.0.0.1) and rank 0 prints the line.
 """
 
 from __future__ import annotations
@@ -24,6 +41,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,24 +56,30 @@ METRIC = "simulated request-steps/sec at 1/2/4/8 B200 vs host-CPU ref; bit-exact
 UNIT = "request-steps/s"
 BYTES_PER_RSTEP = 24  # read {prompt,output,progress,kv} 16 B + write {progress,kv} 8 B
 SEEDS_PER_GPU = 16
+QUARTERS = 4  # the reference arm's per-step sample: one quarter of the sweep
+C5_PREFIX_S = 3600.0  # C5 trace prefix for the bench's c5 figure (~806k requests per cluster)
+C5_SEEDS = 8  # x {sal, rr} = 16 clusters of 64 replicas per GPU
 
 
-def config(world: int) -> dict:
+def config(world: int, scaling: str, n_local: int, dry: bool = False) -> dict:
+    total = 4 * 4 * 16 * SEEDS_PER_GPU * (world if scaling == "weak" else 1)
     return {
         "workload": "C4 policy/config sweep (BASELINE.json configs[3]): {fcfs, nopreempt, trail_plus c=0.5, "
                     "larry a=1} x KV pools {1024, 2048, 4096, 11444} x scale_qps {0.25..4.0 step 0.25} x "
-                    f"{SEEDS_PER_GPU} seeds per GPU; chat-shaped trace 3 qps, burstiness 2, 600 s per seed; "
-                    "llama3-8b/a100 cost model; 1 replica per instance",
-        "instances_per_gpu": 4 * 4 * 16 * SEEDS_PER_GPU,
-        "total_instances": 4 * 4 * 16 * SEEDS_PER_GPU * world,
+                    f"{SEEDS_PER_GPU} seeds; chat-shaped trace 3 qps, burstiness 2, 600 s per seed; "
+                    "llama3-8b/a100 cost model; 1 replica per instance"
+                    + (" [DRY-CPU: 60-s traces, every 16th job, oracle in place of the kernels]" if dry else ""),
+        "scaling_mode": scaling,
+        "instances_this_rank": n_local,
+        "total_instances": total,
         "step": "simulate every instance + exact per-instance Summary (TTFT/nTTFT/TGT/TPOT/queue percentiles)",
-        "parallelism": f"instance-sharded x{world}" + (" + NCCL all_gather of summaries" if world > 1 else ""),
+        "parallelism": f"instance-sharded x{world}" + (" + all_gather of summaries" if world > 1 else ""),
         "l2": "working set (trace+records+scratch, ~1 GB per GPU) exceeds L2; L2 flushed (256 MB write) before "
               "every timed step",
         "schedule": "one persistent kernel; SMs split among (policy, KV-pool class) queues by estimated work, one "
                     "engine copy per policy, longest-first queues, an SM switches policy only when all its warps are "
-                    "drained; estimates = iterations x the policy's mean device cycles per iteration, measured in the "
-                    "untimed first pass",
+                    "drained; value: host cost estimates (what a first run of a sweep gets); warm_schedule: "
+                    "estimates = iterations x the policy's mean device cycles per iteration from an untimed pass",
     }
 
 
@@ -112,15 +136,64 @@ def measured_hbm_peak() -> tuple[float, str]:
 
 def ncu_traffic():
     """dram bytes per k_engines launch from the committed ncu capture (profiles/), or None."""
-    p = ROOT / "profiles" / "r01_k_engines_traffic.json"
-    if p.exists():
-        try:
-            d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
-        except Exception:
-            pass
-    return None, None
+    for name in ("r02_k_engines_traffic.json", "r01_k_engines_traffic.json"):
+        p = ROOT / "profiles" / name
+        if p.exists():
+            try:
+                return json.loads(p.read_text()).get("dram_bytes_per_launch")
+            except Exception:
+                pass
+    return None
 
+
+# --------------------------------------------------------------------------- sharding
+
+def sweep_jobs(scaling: str, rank: int, world: int, dry: bool = False):
+    """This rank's C4 jobs. weak: its own 16 seeds; strong: its LPT share of the one sweep."""
+    from paper_2410_17840_b200 import configs as C
+
+    dur = 60.0 if dry else 600.0
+    if scaling == "weak":
+        jobs = C.c4_jobs(seeds=range(SEEDS_PER_GPU * rank, SEEDS_PER_GPU * (rank + 1)), duration_s=dur)
+        if dry:
+            jobs = jobs[::16]
+        return jobs, len(jobs)
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200.shard import strong_shard
+    from paper_2410_17840_b200.simulate import estimate_cost
+
+    jobs = C.c4_jobs(seeds=range(SEEDS_PER_GPU), duration_s=dur)
+    if dry:
+        jobs = jobs[::16]
+    cost = estimate_cost(I.make_batch(jobs))
+    mine = strong_shard(cost, rank, world)
+    longest = max(len(strong_shard(cost, r, world)) for r in range(world))
+    return [jobs[i] for i in mine], longest
+
+
+def quarter_slices(n: int) -> list:
+    """A fixed random partition of the sweep's instances into QUARTERS equal samples."""
+    import numpy as np
+
+    perm = np.random.default_rng(2410_17840).permutation(n)
+    return [np.sort(perm[k::QUARTERS]) for k in range(QUARTERS)]
+
+
+def sub_batch(batch, idx, longest_first: bool = True):
+    """The instances idx of batch (records keep their offsets), longest estimated first."""
+    import numpy as np
+
+    from paper_2410_17840_b200.instances import Batch
+    from paper_2410_17840_b200.simulate import estimate_cost
+
+    idx = np.asarray(idx)
+    if longest_first:
+        idx = idx[np.argsort(-estimate_cost(batch)[idx], kind="stable")]
+    return Batch(batch.trace, batch.instances[idx].copy(), batch.n_records,
+                 [batch.labels[i] for i in idx]), idx
+
+
+# --------------------------------------------------------------------------- reference arm
 
 def reference_arm(args, rank: int, world: int) -> None:
     """--impl reference: the CPU oracle (port of the reference algorithm) on all host cores."""
@@ -132,55 +205,289 @@ def reference_arm(args, rank: int, world: int) -> None:
 
     O.build()
     threads = os.cpu_count() or 1
-    batch = I.make_batch(C.c4_jobs(seeds=range(1)))
-    times, rs = [], 0
+    full = I.make_batch(C.c4_jobs(seeds=range(SEEDS_PER_GPU)))
+    parts = [sub_batch(full, q)[0] for q in quarter_slices(len(full.instances))]
+    times, rs_tot = [], 0
     for k in range(args.warmup + args.steps):
+        b = parts[k % QUARTERS]
         t0 = time.perf_counter()
-        _, st = O.run_batch(batch, threads=threads)
+        _, st = O.run_batch(b, threads=threads)
         dt = time.perf_counter() - t0
-        rs = int(st["request_steps"].sum())
         if k >= args.warmup:
             times.append(dt)
+            rs_tot += int(st["request_steps"].sum())
     tot = sum(times)
-    value = rs * len(times) / tot
+    value = rs_tot / tot
+    # one pass over the whole sweep in a single queue, longest first (the like-for-like figure)
+    fb, _ = sub_batch(full, range(len(full.instances)))
+    t0 = time.perf_counter()
+    _, st = O.run_batch(fb, threads=threads)
+    dt_full = time.perf_counter() - t0
+    rs_full = int(st["request_steps"].sum())
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64/i32", "data": "synthetic", "config": config(world),
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64/i32", "data": "synthetic",
+        "config": config(world, args.scaling, len(full.instances)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": "seed-0 slice of the sweep: 256 instances (4 policies x 4 pools x 16 rates), "
-                                   f"{rs:,} request-steps per step"},
+                         "sample": f"per step one quarter of the 4,096-instance sweep (fixed random partition, "
+                                   f"1,024 instances, longest estimated first), quarters in rotation; "
+                                   f"{rs_tot:,} request-steps over {len(times)} steps"},
+        "full_sweep": {"value": rs_full / dt_full, "unit": UNIT, "seconds": dt_full, "request_steps": rs_full,
+                       "threads": threads},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_and_parity(runner_stats) -> dict:
-    """Oracle on the host cores over the seed-0 slice (256 instances = the first 256
-    of rank 0's sweep); also checks them bit-exactly against the GPU results."""
+# --------------------------------------------------------------------------- our arm
+
+class GpuSweep:
+    """The product path: SweepRunner (libssb.so) on this rank's GPU."""
+
+    dry = False
+
+    def __init__(self, jobs, pad_rows: int, dist, local: int):
+        import torch
+
+        from paper_2410_17840_b200 import _abi
+        from paper_2410_17840_b200.sweep import SweepRunner
+
+        self.torch, self.dist, self.jobs = torch, dist, jobs
+        self.runner = SweepRunner(jobs)
+        self.device = self.runner.device
+        self.flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=self.device)
+        self.stream = torch.cuda.current_stream()
+        self.row = _abi.SUMMARY.itemsize
+        self.pad = torch.zeros(pad_rows * self.row, dtype=torch.uint8, device=self.device)
+        world = dist.get_world_size() if dist else 1
+        self.gather = torch.empty(world * pad_rows * self.row, dtype=torch.uint8, device=self.device)
+        self.timer_sim = 0.0
+
+    def first_pass(self):
+        r = self.runner
+        r.run()
+        r.results()
+        reruns = r.fix_overflows()
+        stats, _ = r.results()
+        return stats, reruns
+
+    def _gather(self, d_summary):
+        if self.dist is None:
+            return
+        n = d_summary.numel()
+        self.pad[:n].copy_(d_summary)
+        self.dist.all_gather_into_tensor(self.gather, self.pad)
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def kernel_step(self, measure_sim: bool) -> tuple[float, float]:
+        """One sweep, inputs resident; (step seconds, simulate-kernel seconds) by CUDA events."""
+        torch, r = self.torch, self.runner
+        self.flush.fill_(1)
+        self.barrier()
+        e0, e1, s0, s1 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        e0.record(self.stream)
+        s0.record(self.stream)
+        r.simulate()
+        s1.record(self.stream)
+        r.summarize()
+        self._gather(r.d_summary)
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3, s0.elapsed_time(s1) / 1e3
+
+    def e2e_step(self) -> tuple[float, int, int]:
+        """One sweep through the public API from host objects; host clock between syncs
+        (the region holds host planning, so device events alone would not see it)."""
+        from paper_2410_17840_b200.sweep import SweepRunner
+
+        self.flush.fill_(1)
+        self.barrier()
+        t0 = time.perf_counter()
+        r = SweepRunner(self.jobs)
+        r.run()
+        self._gather(r.d_summary)
+        stats, summaries = r.results()
+        dt = time.perf_counter() - t0
+        assert len(summaries) == len(self.jobs)
+        return dt, int(r.h2d_bytes), int(r.d2h_bytes)
+
+    def adopt(self, stats):
+        self.runner.adopt_measured_schedule(stats)
+
+    def reduce(self, x: float, op: str) -> float:
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([x], dtype=torch_dtype(self.torch, x), device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return t.item()
+
+    @property
+    def launches_per_step(self) -> int:
+        return self.runner.launches_per_run
+
+
+def torch_dtype(torch, x):
+    return torch.int64 if isinstance(x, int) else torch.float64
+
+
+class DrySweep:
+    """--dry-cpu: the oracle standing in for the kernels (gloo, host clock). Test plumbing only."""
+
+    dry = True
+
+    def __init__(self, jobs, pad_rows: int, dist, local: int):
+        import numpy as np
+        import torch
+
+        from oracle import oracle as O
+        from paper_2410_17840_b200 import _abi
+        from paper_2410_17840_b200 import instances as I
+
+        self.torch, self.dist, self.jobs, self.O, self.I, self.np = torch, dist, jobs, O, I, np
+        self.batch = I.make_batch(jobs)
+        self.row = _abi.STATS.itemsize
+        self.pad_rows = pad_rows
+        self.device = torch.device("cpu")
+        self.stats = None
+
+    def _run(self, batch):
+        _, st = self.O.run_batch(batch, threads=2)
+        return st
+
+    def _gather(self, st):
+        if self.dist is None:
+            return
+        raw = self.np.zeros(self.pad_rows * self.row, dtype=self.np.uint8)
+        b = st.view(self.np.uint8)
+        raw[:len(b)] = b
+        t = self.torch.from_numpy(raw)
+        outs = [self.torch.empty_like(t) for _ in range(self.dist.get_world_size())]
+        self.dist.all_gather(outs, t)
+        self.gathered = outs
+
+    def first_pass(self):
+        self.stats = self._run(self.batch)
+        return self.stats, 0
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def kernel_step(self, measure_sim: bool):
+        self.barrier()
+        t0 = time.perf_counter()
+        st = self._run(self.batch)
+        t1 = time.perf_counter()
+        self._gather(st)
+        return time.perf_counter() - t0, t1 - t0
+
+    def e2e_step(self):
+        self.barrier()
+        t0 = time.perf_counter()
+        st = self._run(self.I.make_batch(self.jobs))
+        self._gather(st)
+        return time.perf_counter() - t0, 0, 0
+
+    def adopt(self, stats):
+        pass
+
+    def reduce(self, x, op: str):
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([x], dtype=torch_dtype(self.torch, x))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return t.item()
+
+    launches_per_step = 0
+
+
+def cpu_baseline_and_parity(stats, jobs) -> dict:
+    """The oracle on the host cores over one quarter of the sweep (the reference arm's first
+    sample, 1,024 instances); the same instances are checked bit-exactly against the GPU."""
     import numpy as np
 
     from oracle import oracle as O
-    from paper_2410_17840_b200 import configs as C
     from paper_2410_17840_b200 import instances as I
 
     O.build()
     threads = os.cpu_count() or 1
-    batch = I.make_batch(C.c4_jobs(seeds=range(1)))
+    full = I.make_batch(jobs)
+    b, idx = sub_batch(full, quarter_slices(len(full.instances))[0])
     t0 = time.perf_counter()
-    _, st = O.run_batch(batch, threads=threads)
+    _, st = O.run_batch(b, threads=threads)
     dt = time.perf_counter() - t0
     rs = int(st["request_steps"].sum())
-    g = runner_stats[: len(st)]
-    keys = ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "parks", "finished", "digest",
-            "status")
+    g = stats[idx]
+    keys = ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "parks", "finished",
+            "peak_batch_tokens", "digest", "status")
     exact = all(np.array_equal(g[k], st[k]) for k in keys)
     return {
         "cpu_baseline": {"value": rs / dt, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"seed-0 slice of the sweep: 256 instances, {rs:,} request-steps, {dt:.2f} s"},
-        "parity": {"instances_checked": int(len(st)), "bit_exact_vs_oracle": bool(exact),
-                   "fields": list(keys)},
+                         "sample": f"one quarter of the sweep (fixed random partition, longest estimated first): "
+                                   f"{len(idx)} instances, {rs:,} request-steps, {dt:.2f} s"},
+        "parity": {"instances_checked": int(len(idx)), "bit_exact_vs_oracle": bool(exact), "fields": list(keys)},
     }
+
+
+def c5_figure(steps: int) -> dict:
+    """16 independent 64-replica clusters (C5 shape: larry, sal and rr, 224 qps, burstiness 3,
+    seeds 0..7) on a C5_PREFIX_S-second prefix: device time per launch (CUDA events, inputs
+    resident) next to the oracle on the same clusters (all host threads), bit-exact check."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200 import simulate
+
+    jobs = []
+    for s in range(C5_SEEDS):
+        jobs += C.c5_jobs(duration_s=C5_PREFIX_S, seed=s)
+    batch = I.make_batch(jobs)
+    db = simulate.upload(batch)
+    simulate.launch(db)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ts = []
+    for _ in range(max(1, steps)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        simulate.launch(db)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    _, st = simulate.download(db)
+    rs = int(st["request_steps"].sum())
+    threads = os.cpu_count() or 1
+    O.build()
+    t0 = time.perf_counter()
+    _, ost = O.run_batch(batch, threads=threads)
+    dt = time.perf_counter() - t0
+    keys = ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "finished", "digest", "status")
+    t = statistics.median(ts)
+    return {"value": rs / t, "unit": UNIT, "seconds_per_launch": t, "clusters": len(jobs), "replicas": 64,
+            "requests": int(batch.n_records), "request_steps": rs, "prefix_s": C5_PREFIX_S,
+            "oracle": {"value": rs / dt, "seconds": dt, "threads": threads, "kind": "port"},
+            "gpu_over_oracle": dt / t,
+            "bit_exact_vs_oracle": bool(all(np.array_equal(st[k], ost[k]) for k in keys))}
+
+
+def spawn(args) -> int:
+    """--gpus N > 1 outside torchrun: relaunch this script under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def main() -> None:
@@ -189,11 +496,16 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--dry-cpu", action="store_true", help="gloo + oracle plumbing test (not a measurement)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         reference_arm(args, rank, world)
@@ -202,123 +514,77 @@ def main() -> None:
     import numpy as np
     import torch
 
-    torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2410_17840_b200 import configs as C
-    from paper_2410_17840_b200.sweep import SweepRunner
+        if args.dry_cpu:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif not args.dry_cpu:
+        torch.cuda.set_device(local)
 
-    runner = SweepRunner(C.c4_jobs(seeds=range(SEEDS_PER_GPU * rank, SEEDS_PER_GPU * (rank + 1))))
-    # first pass: correctness + overflow re-runs (deterministic: later passes identical)
-    runner.run()
-    stats, _ = runner.results()
-    overflow_reruns = runner.fix_overflows()
-    stats, summaries = runner.results()
-    runner.adopt_measured_schedule(stats)  # placement hint for the next runs
+    jobs, pad_rows = sweep_jobs(args.scaling, rank, world, dry=args.dry_cpu)
+    S = (DrySweep if args.dry_cpu else GpuSweep)(jobs, pad_rows, dist, local)
+    # first pass: correctness + capacity-overflow re-runs (deterministic: later passes identical)
+    stats, overflow_reruns = S.first_pass()
     if (stats["status"] != 0).any():
         raise SystemExit(f"rank {rank}: instance status {np.unique(stats['status'])}")
     rsteps = int(stats["request_steps"].sum())
-    gather = None
-    if world > 1:
-        gather = torch.empty(world * runner.d_summary.numel(), dtype=torch.uint8, device=runner.d_summary.device)
-
-    def step(e2e: bool):
-        runner.run(copy_inputs=e2e, read_results=False)
-        if gather is not None:
-            dist.all_gather_into_tensor(gather, runner.d_summary)
-        if e2e:
-            runner.read_results()
-
     for _ in range(args.warmup):
-        step(False)
-        step(True)
-    torch.cuda.synchronize()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=runner.device)
-    stream = torch.cuda.current_stream()
+        S.kernel_step(False)
+    S.e2e_step()
 
-    def timed(e2e: bool, measure_sim: bool):
-        tot = sim = 0.0
-        for _ in range(args.steps):
-            flush.fill_(1)
-            torch.cuda.synchronize()
-            if dist is not None:
-                dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            if e2e:
-                runner.copy_inputs()
-            if measure_sim:
-                s0.record(stream)
-            runner.simulate()
-            if measure_sim:
-                s1.record(stream)
-            runner.summarize()
-            if gather is not None:
-                dist.all_gather_into_tensor(gather, runner.d_summary)
-            if e2e:
-                runner.read_results()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            tot += e0.elapsed_time(e1) / 1e3
-            if measure_sim:
-                sim += s0.elapsed_time(s1) / 1e3
-        return tot, sim
+    clk = ClockSampler(local) if not args.dry_cpu else None
+    K = args.steps
+    cold = [S.kernel_step(True) for _ in range(K)]
+    e2e = [S.e2e_step() for _ in range(K)]
+    S.adopt(stats)  # placement from the measured costs (identical work and results)
+    S.kernel_step(False)
+    warm = [S.kernel_step(True) for _ in range(K)]
+    clocks = clk.stop() if clk else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["dry-cpu"]}
 
-    clk = ClockSampler(local)
-    t_kernel, t_sim = timed(False, True)
-    t_e2e, _ = timed(True, False)
-    clocks = clk.stop()
-    st2, _ = runner.results()  # the e2e steps copied the results back: still the first pass's
-    assert np.array_equal(st2["digest"], stats["digest"]), "results changed between steps"
-
-    def max_over_ranks(x: float) -> float:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=runner.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x: int) -> int:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.int64, device=runner.device)
-        dist.all_reduce(t)
-        return int(t.item())
-
-    T_kernel, T_e2e, T_sim = max_over_ranks(t_kernel), max_over_ranks(t_e2e), max_over_ranks(t_sim)
-    total_rsteps = sum_over_ranks(rsteps)
+    T_cold = S.reduce(sum(t for t, _ in cold), "max")
+    T_sim = S.reduce(sum(s for _, s in cold), "max")
+    T_warm = S.reduce(sum(t for t, _ in warm), "max")
+    T_e2e = S.reduce(sum(t for t, _, _ in e2e), "max")
+    total_rsteps = int(S.reduce(rsteps, "sum"))
     if rank == 0:
-        K = args.steps
-        value = total_rsteps * K / T_kernel
-        e2e_value = total_rsteps * K / T_e2e
+        value = total_rsteps * K / T_cold
         sim_s = T_sim / K
         achieved = BYTES_PER_RSTEP * rsteps / sim_s / 1e9  # per launch on this rank
         peak, peak_src = measured_hbm_peak()
-        traffic, _alg = ncu_traffic()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": 1e3 * T_kernel / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64/i32", "data": "synthetic", "config": config(world),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(runner.h2d_bytes),
-                    "d2h_bytes_per_step": int(runner.d2h_bytes), "ms_per_step": 1e3 * T_e2e / K,
-                    "api": "paper_2410_17840_b200.sweep.SweepRunner.run"},
+            "ms_per_step": 1e3 * T_cold / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f64/i32", "data": "synthetic", "config": config(world, args.scaling, len(jobs), args.dry_cpu),
+            "e2e": {"value": total_rsteps * K / T_e2e, "unit": UNIT, "h2d_bytes_per_step": e2e[0][1],
+                    "d2h_bytes_per_step": e2e[0][2], "ms_per_step": 1e3 * T_e2e / K,
+                    "api": "paper_2410_17840_b200.sweep.SweepRunner(jobs) + .run() + .results(): validation, "
+                           "feasibility, planning, H2D, simulate, summarise, D2H (host clock, max over ranks)"},
+            "warm_schedule": {"value": total_rsteps * K / T_warm, "ms_per_step": 1e3 * T_warm / K,
+                              "note": "after one untimed pass fed back each instance's measured cost (placement "
+                                      "only; same work, same results)"},
             "roofline": {"bound": "hbm", "kernel": "k_engines (ssb_simulate)", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(),
                          "algorithmic_bytes": f"{BYTES_PER_RSTEP} B/request-step x {rsteps:,} request-steps",
-                         "kernel_ms": 1e3 * sim_s, "kernel_share_of_step": sim_s / (T_kernel / K),
+                         "kernel_ms": 1e3 * sim_s, "kernel_share_of_step": sim_s / (T_cold / K),
                          "peak_source": peak_src},
-            "gpu_launches": runner.launches_per_run * K * 2,
+            "gpu_launches": S.launches_per_step * K * 3,  # cold + e2e + warm steps
             "clocks": clocks,
             "request_steps_per_gpu_step": rsteps,
-            "requests_per_gpu_step": int(runner.batch.n_records),
+            "request_steps_total_per_step": total_rsteps,
             "overflow_reruns": overflow_reruns,
         }
-        if world == 1 and not args.no_cpu_baseline:
-            line.update(cpu_baseline_and_parity(stats))
+        if args.dry_cpu:
+            line["dry_cpu"] = "gloo + oracle in place of the kernels: a plumbing test, not a measurement"
+        elif world == 1 and args.scaling == "weak":
+            if not args.no_cpu_baseline:
+                line.update(cpu_baseline_and_parity(stats, jobs))
+            if not args.no_c5:
+                line["c5"] = c5_figure(min(K, 3))
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -212,14 +212,19 @@ int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* d_inst, int
                      ssb_event* d_events, int64_t event_cap, int64_t* d_event_count,
                      void* stream /* cudaStream_t */);
 
-/* After ssb_simulate (same stream, same scratch): per-engine counters of every
- * instance. Row (i, s) = instance i's server s is written to
- * d_out[d_engine_offset[i] + s] (d_engine_offset: device array of n_inst row
- * offsets, typically the exclusive prefix sum of n_servers). Replaces reading
- * engine.iterations / engine.peak_batch_tokens off the engines passed to
- * run_cluster(..., engines=...) (cluster.py:66-79). */
+/* After ssb_simulate (same stream, same scratch, stats, records and event counts):
+ * per-engine counters of every instance. Row (i, s) = instance i's server s is
+ * written to d_out[d_engine_offset[i] + s] (d_engine_offset: device array of n_inst
+ * row offsets, typically the exclusive prefix sum of n_servers). A cluster's
+ * servers keep their state in the scratch buffer; a single-server instance's row
+ * is its ssb_stats (digest unfolded), its clock the time of its last step (= its
+ * latest finish: the last step finishes the last request, engine.py:256-265) and
+ * its event count d_event_count[i] (NULL when no events were recorded: 0).
+ * Replaces reading engine.iterations / engine.peak_batch_tokens / engine.clock off
+ * the engines passed to run_cluster(..., engines=...) (cluster.py:66-79). */
 int32_t ssb_engine_stats_gather(const ssb_instance* h_inst, const ssb_instance* d_inst, int32_t n_inst,
-                                const void* d_scratch, const int64_t* d_engine_offset,
+                                const void* d_scratch, const ssb_stats* d_stats, ssb_records records,
+                                const int64_t* d_event_count, const int64_t* d_engine_offset,
                                 ssb_engine_stats* d_out, void* stream);
 
 /* One summary group = one summarize(records) call (metrics.py:80-99) over

@@ -230,8 +230,8 @@ EXPORTS = {
     "ssb_struct_sizes": (ctypes.c_int32, [ctypes.c_void_p]),
     "ssb_engine_stats_gather": (
         ctypes.c_int32,
-        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-         ctypes.c_void_p],
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, SsbRecords,
+         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
     ),
 }
 

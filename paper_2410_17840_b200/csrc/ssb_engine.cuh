@@ -37,6 +37,7 @@ constexpr int ST_DECODE = 2;   // RequestState.DECODING
 constexpr int FLAG_SEEN = (int)0x80000000;  // waiting entry was dispatched before (preempted/parked)
 constexpr unsigned long long FNV_OFF = 0xcbf29ce484222325ULL;
 constexpr unsigned long long FNV_PRIME = 0x100000001b3ULL;
+constexpr unsigned long long FNV_PRIME_INV = 0xce965057aff6957bULL;  // FNV_PRIME^-1 mod 2^64
 
 // trail_plus waiting set geometry: one bucket per remaining-output value
 // (remaining <= output_len < min(max_context, pool tokens), policies.py:56-68 feasibility),

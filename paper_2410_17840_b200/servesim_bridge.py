@@ -147,6 +147,7 @@ class _Device:
         t = self.torch
         self.d_ev = (t.empty(len(self.inst) * self.event_cap * _abi.EVENT.itemsize, dtype=t.uint8, device=self.dev)
                      if self.event_cap else None)
+        self.d_evc = t.zeros(max(len(self.inst), 1), dtype=t.int64, device=self.dev)  # events per instance
 
     def trace_c(self):
         return _abi.SsbTrace(self.d_arr.data_ptr(), self.d_prm.data_ptr(), self.d_out.data_ptr())
@@ -163,7 +164,7 @@ class _Device:
         rc = self.lib.ssb_simulate(self.inst.ctypes.data, d_inst.data_ptr(), len(self.inst), self.trace_c(),
                                    self.records_c(), self.d_stats.data_ptr(), self.d_scratch.data_ptr(),
                                    self.scratch_bytes, self.d_ev.data_ptr() if self.d_ev is not None else None,
-                                   self.event_cap, None, self._stream())
+                                   self.event_cap, self.d_evc.data_ptr(), self._stream())
         if rc != 0:
             raise RuntimeError(f"ssb_simulate: {self.lib.ssb_error_string(rc).decode()}")
         self.d_inst = d_inst
@@ -198,7 +199,8 @@ class _Device:
         out = self.torch.empty(int(self.rows[-1]) * _abi.ENGINE_STATS.itemsize, dtype=self.torch.uint8,
                                device=self.dev)
         rc = self.lib.ssb_engine_stats_gather(self.inst.ctypes.data, self.d_inst.data_ptr(), len(self.inst),
-                                              self.d_scratch.data_ptr(), self.d_rows.data_ptr(), out.data_ptr(),
+                                              self.d_scratch.data_ptr(), self.d_stats.data_ptr(), self.records_c(),
+                                              self.d_evc.data_ptr(), self.d_rows.data_ptr(), out.data_ptr(),
                                               self._stream())
         if rc != 0:
             raise RuntimeError(f"ssb_engine_stats_gather: {self.lib.ssb_error_string(rc).decode()}")

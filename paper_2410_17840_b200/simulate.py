@@ -33,15 +33,88 @@ def _np_to_dev(torch, arr: np.ndarray, device):
     return t.to(device, non_blocking=False)
 
 
+def cost_features(batch: Batch) -> np.ndarray:
+    """Per instance (n requests, offered load rho, estimated iterations), from the trace and
+    the engine parameters alone -- no simulation. A fluid model of one engine: requests
+    arrive at lam = n / (arrival span / qps_factor), each decodes mean(output) steps, so
+    by Little's law the running set holds R = lam * mean(output) * L(R) requests, with
+    L(R) = overhead + max(mem_base + mem_per_kv * R * ctx, compute * R) the step latency
+    (costmodel.py:37-47) and ctx = mean(prompt + output / 2), inflated by the prefill share
+    lam * mean(prompt) * compute; R is capped by the pool (pool tokens / ctx, or for
+    nopreempt / the worst-case reservation min(max_context, prompt + max_output),
+    policies.py:116-117). rho = the load at that cap; iterations = Σ(output + 1) / R."""
+    inst = batch.instances
+    tr = batch.trace
+    n_inst = len(inst)
+    out = np.zeros((n_inst, 3))
+    if n_inst == 0:
+        return out
+    o = inst["trace_offset"].astype(np.int64)
+    n = inst["n_requests"].astype(np.int64)
+    p = tr.prompt.astype(np.float64)
+    q = tr.output.astype(np.float64)
+    cp = np.concatenate([[0.0], np.cumsum(p)])
+    cq = np.concatenate([[0.0], np.cumsum(q)])
+    e = inst["engine"]
+    mo = e["max_output"].astype(np.float64)
+    mc = e["max_context"].astype(np.float64)
+    nz = np.maximum(n, 1)
+    psum, qsum = cp[o + n] - cp[o], cq[o + n] - cq[o]
+    pm, qm = psum / nz, qsum / nz
+    ctx = pm + qm / 2
+    # nopreempt: mean reservation, min(max_context, prompt + max_output) per request
+    res = ctx.copy()
+    for i in np.flatnonzero(e["policy"] == 1):
+        seg = p[o[i]:o[i] + n[i]]
+        res[i] = np.minimum(mc[i], seg + mo[i]).mean() if n[i] else ctx[i]
+    last = np.where(n > 0, tr.arrival[np.minimum(o + np.maximum(n - 1, 0), max(len(tr.arrival) - 1, 0))], 0.0)
+    first = np.where(n > 0, tr.arrival[np.minimum(o, max(len(tr.arrival) - 1, 0))], 0.0)
+    span = np.maximum((last - first) / inst["qps_factor"], 1e-9)
+    lam = nz / span
+    rmax = np.maximum(1.0, e["pool_blocks"] * e["block_size"] / np.maximum(res, 1.0))
+    oh, mb, mkv, cpt = e["overhead_s"], e["mem_base_s"], e["mem_per_kv_token_s"], e["compute_per_token_s"]
+    pre = 1.0 / np.maximum(0.05, 1.0 - lam * pm * cpt)  # prefill share of the engine's time
+    R = np.ones(n_inst)
+    for _ in range(60):
+        L = oh + np.maximum(mb + mkv * R * ctx, cpt * R)
+        R = np.minimum(rmax, 0.5 * R + 0.5 * np.maximum(1.0, lam * qm * L * pre))
+    Lmax = oh + np.maximum(mb + mkv * rmax * ctx, cpt * rmax)
+    out[:, 0] = nz
+    out[:, 1] = np.maximum(lam * qm * Lmax * pre / rmax, 1e-3)
+    out[:, 2] = np.maximum((qsum + n) / R, 1.0)
+    return out
+
+
+# log(device cycles) ~ c0 + c1 log n + c2 log rho + c3 log iterations + c4 (log rho)^2, per policy
+# (fcfs, nopreempt, trail_plus, larry); least squares on the device cycles of a C4 sweep of
+# seeds 100-115 (not the bench's 0-15) on one B200: tools/fit_cost_model.py,
+# profiles/r02_cost_model.json. Only the placement uses it: results never depend on it.
+COST_COEF = np.array([
+    [9.857, 1.088, -0.104, -0.117, 0.033],
+    [7.520, 0.585, 0.045, 0.468, -0.007],
+    [12.187, 0.488, 0.411, 0.248, -0.061],
+    [8.767, 0.893, 0.213, 0.200, -0.003],
+])
+
+
 def estimate_cost(batch: Batch) -> np.ndarray:
-    """Scheduling hint ~ request-steps: Σ output tokens (+ prompt chunks) per instance."""
-    out = np.zeros(len(batch.instances), dtype=np.int64)
-    csum = np.concatenate([[0], np.cumsum(batch.trace.output.astype(np.int64) + 1)])
-    for i, inst in enumerate(batch.instances):
-        o, n = int(inst["trace_offset"]), int(inst["n_requests"])
-        f = float(inst["engine"]["policy"] == 1) * 4 + 1  # nopreempt steps are slow under backlog
-        out[i] = int((csum[o + n] - csum[o]) * f)
-    return np.clip(out // 16, 0, 2**31 - 1)
+    """Scheduling hint (estimated device cycles / 1024, the unit of measured_cost) for a
+    first run: the per-policy cost model above over cost_features. Clusters (n_servers > 1)
+    keep a work proxy (Σ output tokens): they run one per thread-block cluster."""
+    inst = batch.instances
+    if len(inst) == 0:
+        return np.zeros(0, dtype=np.int64)
+    f = cost_features(batch)
+    ln, lr, li = np.log(f[:, 0]), np.log(f[:, 1]), np.log(f[:, 2])
+    X = np.stack([np.ones(len(f)), ln, lr, li, lr * lr], 1)
+    pol = inst["engine"]["policy"].astype(np.int64) & 3
+    cyc = np.exp(np.einsum("ij,ij->i", X, COST_COEF[pol]))
+    multi = inst["n_servers"] > 1
+    if multi.any():
+        csum = np.concatenate([[0], np.cumsum(batch.trace.output.astype(np.int64) + 1)])
+        o, n = inst["trace_offset"].astype(np.int64), inst["n_requests"].astype(np.int64)
+        cyc[multi] = (csum[o + n] - csum[o])[multi] * 1024.0
+    return np.clip(cyc / 1024.0, 1, 2**31 - 1).astype(np.int64)
 
 
 def measured_cost(h_inst: np.ndarray, stats: np.ndarray) -> np.ndarray | None:
@@ -154,7 +227,9 @@ def engine_stats(db: DeviceBatch, stream=None) -> np.ndarray:
         stream = torch.cuda.current_stream()
     out = torch.empty(max(db.n_engines, 1) * _abi.ENGINE_STATS.itemsize, dtype=torch.uint8, device=db.d_inst.device)
     rc = lib.ssb_engine_stats_gather(db.h_inst.ctypes.data, db.d_inst.data_ptr(), len(db.h_inst),
-                                     db.d_scratch.data_ptr(), db.d_engine_offset.data_ptr(), out.data_ptr(),
+                                     db.d_scratch.data_ptr(), db.d_stats.data_ptr(), db.records_c(),
+                                     db.d_evcount.data_ptr() if db.d_evcount is not None else None,
+                                     db.d_engine_offset.data_ptr(), out.data_ptr(),
                                      ctypes.c_void_p(stream.cuda_stream))
     if rc != 0:
         raise SimulationError(f"ssb_engine_stats_gather: {lib.ssb_error_string(rc).decode()} ({rc})")
