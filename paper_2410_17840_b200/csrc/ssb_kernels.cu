@@ -228,6 +228,19 @@ __global__ void k_scale_arrivals(const ssb_instance* __restrict__ inst, int n_in
   }
 }
 
+#ifdef SSB_TIMELINE
+// debug build only (tools/probe_timeline.py): per single-server instance the %globaltimer
+// ns at start and end and the SM it ran on, read back with ssb_debug_timeline
+constexpr int TIMELINE_MAX = 1 << 16;
+__device__ unsigned long long g_timeline[3 * TIMELINE_MAX];
+#endif
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned sm_id();
+
 // ------------------------------------------------------------------------
 // single-server instances: one warp each, persistent
 // ------------------------------------------------------------------------
@@ -241,6 +254,9 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
                                              int64_t* ev_count, int* sm_tab) {
   const int lane = lane_id();
   const long long t0 = clock64();
+#ifdef SSB_TIMELINE
+  const unsigned long long g0 = globaltimer_ns();
+#endif
   const ssb_instance I = inst[idx];
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;  // compile-time policy: this copy of the engine holds only POL's code
@@ -273,6 +289,11 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
     s.device_cycles = clock64() - t0;
     stats[idx] = s;
     if (ev_count) ev_count[idx] = E.st.ev_n;
+#ifdef SSB_TIMELINE
+    g_timeline[3 * idx] = g0;
+    g_timeline[3 * idx + 1] = globaltimer_ns();
+    g_timeline[3 * idx + 2] = sm_id();
+#endif
   }
   __syncwarp();
 }
@@ -1129,3 +1150,10 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   }
   return SSB_OK;
 }
+
+#ifdef SSB_TIMELINE
+extern "C" int32_t ssb_debug_timeline(unsigned long long* out, int32_t n) {
+  if (n > TIMELINE_MAX) n = TIMELINE_MAX;
+  return cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 3 * (size_t)n) == cudaSuccess ? n : -1;
+}
+#endif
