@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import functools
+
 import numpy as np
 
 
@@ -121,6 +123,17 @@ def make_balancer(name: str, n_servers: int, *, max_tokens_per_batch: int = 1024
 
 def pcg64_words(seed) -> tuple[int, int, int, int]:
     """(state_hi, state_lo, inc_hi, inc_lo) of np.random.default_rng(seed) (cluster.py:94)."""
+    if isinstance(seed, int) and seed >= 0:
+        return _pcg64_words_int(seed)
+    return _pcg64_words(seed)
+
+
+@functools.lru_cache(maxsize=4096)
+def _pcg64_words_int(seed: int) -> tuple[int, int, int, int]:
+    return _pcg64_words(seed)
+
+
+def _pcg64_words(seed) -> tuple[int, int, int, int]:
     st = np.random.PCG64(seed).state["state"]
     s, inc = int(st["state"]), int(st["inc"])
     m = (1 << 64) - 1

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _abi
 from . import instances as I
-from .metrics import MetricsRecord, RecordsSoA, Summary, SummaryExtras, summary_groups, summarize_device, _summary_from_row
+from .metrics import MetricsRecord, RecordsSoA, Summary, SummaryExtras, instance_groups, summarize_device, _summary_from_row
 from .policies import EngineLimits
 from .settings import ClusterSettings, CostParams, EngineSettings, KvBlockPool
 from .workload import Trace, as_trace
@@ -156,10 +156,8 @@ def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, valida
     srows = None
     if summaries:
         inst = db.h_inst
-        groups = summary_groups([(int(i["record_offset"]), int(i["n_requests"])) for i in inst],
-                                trace_offsets=[int(i["trace_offset"]) for i in inst],
-                                qps=[float(i["qps_factor"]) for i in inst])
-        ok = np.array([int(i["n_requests"]) > 0 for i in inst])
+        groups = instance_groups(inst)
+        ok = inst["n_requests"] > 0
         srows = np.zeros(len(inst), dtype=_abi.SUMMARY)
         if ok.any():
             srows[ok] = summarize_device(db.trace_c(), db.records_c(), groups[ok])

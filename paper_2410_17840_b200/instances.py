@@ -70,7 +70,7 @@ def engine_params_record(re: ResolvedEngine) -> np.void:
 def check_qps_factor(qps_factor: float) -> float:
     """scale_qps's argument check (workload.py:187-194)."""
     f = float(qps_factor)
-    if not f > 0 or not np.isfinite(f):
+    if not f > 0 or not math.isfinite(f):
         raise ValueError(f"factor must be > 0, got {qps_factor}")
     return f
 
@@ -179,13 +179,15 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
         sk = id(settings)
         if sk not in base:  # build_engine first (cluster.py:74-79), the balancer after the checks (:96-104)
             keep_alive.append(settings)
-            base[sk] = [resolve_engine(settings.engine), None]
+            r = resolve_engine(settings.engine)
+            lim = r.limits
+            base[sk] = [r, None, (policy_descriptor(r.policy), r.block_size, r.pool_blocks,
+                                  lim.max_tokens_per_batch, lim.max_running, lim.max_context)]
         re = base[sk][0]
         factor = check_qps_factor(factor)
         if validate:
             lim = re.limits
-            fk = (ti, policy_descriptor(re.policy), re.block_size, re.pool_blocks, lim.max_tokens_per_batch,
-                  lim.max_running, lim.max_context)
+            fk = (ti, base[sk][2])
             if fk not in feasible:
                 re.policy.check_feasible_many(t.prompt, t.output, re.block_size, re.pool_blocks, lim)
                 feasible.add(fk)

@@ -151,16 +151,26 @@ def nearest_ranks(n: int) -> tuple[int, int, int]:
 
 
 def summary_groups(offsets_n, trace_offsets=None, qps=None) -> np.ndarray:
-    """ssb_summary_group array for consecutive record groups [(record_offset, n), ...]."""
-    g = np.zeros(len(offsets_n), dtype=_abi.SUMMARY_GROUP)
-    for i, (off, n) in enumerate(offsets_n):
-        g[i]["record_offset"] = off
-        g[i]["trace_offset"] = off if trace_offsets is None else trace_offsets[i]
-        g[i]["n"] = n
-        g[i]["qps_factor"] = 1.0 if qps is None else qps[i]
-        g[i]["rank"][:3] = nearest_ranks(n)
-        g[i]["rank"][3:] = 0  # TPOT ranks: derived on the device from the TPOT sample size
+    """ssb_summary_group array for consecutive record groups [(record_offset, n), ...].
+    The nearest ranks are ceil(p/100*n) in binary64 exactly as Python computes them
+    (metrics.py:53): p/100 and the product round the same way in numpy's float64."""
+    on = np.asarray(offsets_n, dtype=np.int64).reshape(-1, 2)
+    g = np.zeros(len(on), dtype=_abi.SUMMARY_GROUP)
+    g["record_offset"] = on[:, 0]
+    g["trace_offset"] = on[:, 0] if trace_offsets is None else np.asarray(trace_offsets, dtype=np.int64)
+    g["n"] = on[:, 1]
+    g["qps_factor"] = 1.0 if qps is None else np.asarray(qps, dtype=np.float64)
+    nf = on[:, 1].astype(np.float64)
+    for j, p in enumerate((50, 95, 99)):
+        g["rank"][:, j] = np.ceil((p / 100) * nf)
+    # TPOT ranks (3:) stay 0: derived on the device from the TPOT sample size
     return g
+
+
+def instance_groups(inst: np.ndarray) -> np.ndarray:
+    """summary_groups for every row of an INSTANCE array (one group per instance)."""
+    return summary_groups(np.stack([inst["record_offset"], inst["n_requests"]], 1),
+                          trace_offsets=inst["trace_offset"], qps=inst["qps_factor"])
 
 
 def summarize_device(d_trace: _abi.SsbTrace, d_records: _abi.SsbRecords, groups: np.ndarray, device=None):

@@ -166,10 +166,9 @@ def host_hist_fn(values: dict, preempt_count: np.ndarray):
 def pooled_summary_device(runner_or_db, dist=None) -> dict:
     """Pooled percentiles over every instance of a resident batch on this rank (and,
     with ``dist``, over every rank's batch): one ssb_pool_hist + one all-gather per pass."""
-    from .metrics import summary_groups
+    from .metrics import instance_groups
 
     db = getattr(runner_or_db, "db", runner_or_db)
     h = db.h_inst
-    g = summary_groups([(int(i["record_offset"]), int(i["n_requests"])) for i in h],
-                       trace_offsets=[int(i["trace_offset"]) for i in h], qps=[float(i["qps_factor"]) for i in h])
+    g = instance_groups(h)
     return pooled_select(device_hist_fn(db.trace_c(), db.records_c(), g), dist)

@@ -219,11 +219,9 @@ class _Device:
 
     def summaries(self):
         """ssb_summarize over every instance (metrics.py:80-99)."""
-        from .metrics import summary_groups
+        from .metrics import instance_groups
 
-        g = np.ascontiguousarray(summary_groups(
-            [(int(r["record_offset"]), int(r["n_requests"])) for r in self.inst],
-            trace_offsets=[int(r["trace_offset"]) for r in self.inst], qps=[float(r["qps_factor"]) for r in self.inst]))
+        g = np.ascontiguousarray(instance_groups(self.inst))
         d_g = self.torch.from_numpy(g.view(np.uint8)).to(self.dev)
         wb = int(self.lib.ssb_summary_work_bytes(g.ctypes.data, len(g)))
         work = self.torch.empty(max(wb, 8), dtype=self.torch.uint8, device=self.dev)

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _abi
 from . import instances as I
-from .metrics import summary_groups
+from .metrics import instance_groups
 from .simulate import DeviceBatch, SimulationError, estimate_cost, retry_overflows
 
 SUMMARY_LAUNCHES = 18  # k_init + 8 x (k_hist + k_select) + k_finish
@@ -56,9 +56,7 @@ class SweepRunner:
             d_stats=torch.zeros(len(h_inst) * _abi.STATS.itemsize, dtype=torch.uint8, device=dev),
             d_scratch=torch.empty(max(self.scratch_bytes, 256), dtype=torch.uint8, device=dev),
             scratch_bytes=self.scratch_bytes)
-        g = summary_groups([(int(i["record_offset"]), int(i["n_requests"])) for i in h_inst],
-                           trace_offsets=[int(i["trace_offset"]) for i in h_inst],
-                           qps=[float(i["qps_factor"]) for i in h_inst])
+        g = instance_groups(h_inst)
         self.h_groups = np.ascontiguousarray(g)
         self.d_groups = torch.from_numpy(self.h_groups.view(np.uint8)).to(dev)
         wb = int(self.lib.ssb_summary_work_bytes(self.h_groups.ctypes.data, len(g)))

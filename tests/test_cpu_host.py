@@ -174,3 +174,20 @@ def test_simulation_path_fails_loudly_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(Exception, match="CUDA"):
         P.run_cluster(P.ClusterSettings(), [P.TraceEntry(0.0, 10, 1)])
+
+
+def test_vectorised_summary_ranks_equal_python_nearest_rank():
+    """summary_groups computes ceil(p/100*n) in numpy float64; it must equal the
+    reference's Python-float nearest rank (metrics.py:53) for every n."""
+    import math
+
+    import numpy as np
+
+    from paper_2410_17840_b200.metrics import summary_groups
+
+    ns = np.concatenate([np.arange(1, 5000), np.array([10**6, 10**7 + 3, 2**31 - 1, 123456789])])
+    g = summary_groups(np.stack([np.zeros_like(ns), ns], 1))
+    for j, p in enumerate((50, 95, 99)):
+        want = np.array([math.ceil(p / 100 * int(n)) for n in ns])
+        assert np.array_equal(g["rank"][:, j], want), p
+    assert (g["rank"][:, 3:] == 0).all()
