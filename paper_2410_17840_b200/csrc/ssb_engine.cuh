@@ -504,8 +504,10 @@ struct Eng {
       int rid = 0;
       bool ok = false;
       if (valid) {
+        // route-list slots not yet written read as -1 (the pipelined cluster kernel presets
+        // them; every arrival before the engine's time limit is routed and visible)
         rid = (cfg.n_servers == 1) ? k : p.rl[k];
-        ok = arrival_of(rid) <= st.clock;
+        ok = rid >= 0 && arrival_of(rid) <= st.clock;
       }
       unsigned m = __ballot_sync(FULL, ok);  // a prefix: routes are in arrival order
       int cnt = __popc(m);
@@ -1639,13 +1641,31 @@ struct Eng {
   __device__ __forceinline__ double next_arrival(int n_avail) const {
     if (st.next_arr >= n_avail) return __longlong_as_double(0x7ff0000000000000LL);  // +inf: none routed yet
     int rid = (cfg.n_servers == 1) ? st.next_arr : p.rl[st.next_arr];
-    return arrival_of(rid);
+    return rid >= 0 ? arrival_of(rid) : __longlong_as_double(0x7ff0000000000000LL);  // -1: not routed yet
   }
+  // one call per engine lifetime (k_engines) or per routing epoch (k_cluster): the engine is
+  // rebound from memory, so the per-engine modes start fresh and the table is written back
   __device__ __forceinline__ void advance(double t_lim, int n_avail) {
 #ifdef SSB_PHASE_TIMING
     for (int i = 0; i < 16; ++i) tm[i] = tc[i] = 0;
 #endif
     init_modes();
+    advance_loop(t_lim, n_avail);
+    drop_regs();  // the table in memory is authoritative between calls
+#ifdef SSB_PHASE_TIMING
+    if (lane == 0)
+      printf("PHASES iters %lld | enq %lld/%lld | sel %lld/%lld | disp %lld/%lld | fast %lld/%lld | small %lld/%lld | gen %lld/%lld | walk %lld/%lld | victims %lld/%lld\n",
+             st.iterations, tm[0], tc[0], tm[1], tc[1], tm[2], tc[2], tm[3], tc[3], tm[4], tc[4], tm[5], tc[5], tm[6], tm[7], tc[6], tc[7]);
+    if (lane == 0)
+      printf("PHASES2 vbuild %lld/%lld | tfind %lld/%lld | walk %lld/%lld | remove %lld/%lld | vtake %lld/%lld | preempt %lld/%lld | small->gen %lld\n",
+             tm[8], tc[8], tm[9], tc[9], tm[10], tc[10], tm[11], tc[11], tm[12], tc[12], tm[13], tc[13], tc[14]);
+#endif
+  }
+  // the boundary loop: every boundary with time < t_lim. A warp that keeps its engine bound
+  // across calls (k_cluster_pipe) calls this directly: the steady-state register cache, the
+  // nodisp / larry certificates stay valid between calls, because only enqueue_ready (which
+  // resets them) changes what they depend on.
+  __device__ __forceinline__ void advance_loop(double t_lim, int n_avail) {
     double next_t = next_arrival(n_avail);
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
     while (st.status == SSB_OK) {
@@ -1672,15 +1692,6 @@ struct Eng {
       if (regs_ok && nodisp && st.status == SSB_OK && cfg.bs_shift >= 0)
         fast_forward(next_t < t_lim ? next_t : t_lim);
     }
-    drop_regs();  // the table in memory is authoritative between calls
-#ifdef SSB_PHASE_TIMING
-    if (lane == 0)
-      printf("PHASES iters %lld | enq %lld/%lld | sel %lld/%lld | disp %lld/%lld | fast %lld/%lld | small %lld/%lld | gen %lld/%lld | walk %lld/%lld | victims %lld/%lld\n",
-             st.iterations, tm[0], tc[0], tm[1], tc[1], tm[2], tc[2], tm[3], tc[3], tm[4], tc[4], tm[5], tc[5], tm[6], tm[7], tc[6], tc[7]);
-    if (lane == 0)
-      printf("PHASES2 vbuild %lld/%lld | tfind %lld/%lld | walk %lld/%lld | remove %lld/%lld | vtake %lld/%lld | preempt %lld/%lld | small->gen %lld\n",
-             tm[8], tc[8], tm[9], tc[9], tm[10], tc[10], tm[11], tc[11], tm[12], tc[12], tm[13], tc[13], tc[14]);
-#endif
   }
 };
 

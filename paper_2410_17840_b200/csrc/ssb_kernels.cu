@@ -852,6 +852,545 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
   }
 }
 
+// ------------------------------------------------------------------------
+// multi-server instances, pipelined (k_cluster_pipe): one thread-block cluster per
+// instance with a dedicated routing warp (warp 0 of rank 0) and one engine warp per
+// replica (server s = cluster warp s + 1), n <= PIPE_MAX_SERVERS
+// ------------------------------------------------------------------------
+// The classic k_cluster alternates a routing phase and an advance phase with two cluster
+// barriers per epoch, so an epoch costs route + advance + barriers. Here they overlap: an
+// engine never needs more than "every arrival before my next boundary is routed"
+// (cluster.py:128-157: arrivals precede boundaries at equal times), so the router publishes
+// a watermark wt = the time of the first unrouted arrival and every engine advances through
+// its boundaries < wt while the router routes on. Only a route that reads engine state (a
+// p2c/sal poll refresh, a sal route whose argmin depends on beta) needs the engines at
+// exactly its time t: the router publishes wt = t with the sync bit, waits until every
+// engine has reached t and published its ground-truth snapshot (snapshot_stats,
+// cluster.py:50-59, 110-120), and reads the snapshots.
+//
+// All router <-> engine traffic is in shared memory, each datum written by its owner into
+// its own CTA's shared memory and read by the other side over DSMEM, so the release is
+// fence.release.sync_restrict::shared::cta.cluster (MEMBAR.ALL.CTA in SASS) and the acquire
+// fence.acquire.sync_restrict::shared::cluster.cluster (no instruction): no global-scope
+// fence and no L1 invalidation (a fence.acq_rel.cluster is MEMBAR.ALL.GPU + CCTL.IVALL,
+// which flushed the engines' L1 at every wake in a first version).
+//   router -> engine: per server a ring of routed arrival ids and its published count in
+//     rank 0, the watermark word pushed into each CTA, a wake hint (the count) pushed next
+//     to it; the engine copies new ids into its own global route list and reports how far
+//     it has taken (flow control: the router waits before overwriting an untaken slot).
+//   engine -> router: at a sync the snapshot in the engine's CTA, then its done word pushed
+//     into rank 0.
+constexpr int PIPE_WARPS = 8;
+constexpr int PIPE_MAX_CTAS = 16;  // non-portable cluster size (cudaFuncAttributeNonPortableClusterSizeAllowed)
+constexpr int PIPE_MAX_SERVERS = PIPE_WARPS * PIPE_MAX_CTAS - 1;
+constexpr int PIPE_RING = 128;     // routed ids in flight per server (>= 32: one route-log flush)
+constexpr unsigned long long SYNC_BIT = 0x8000000000000000ULL;  // watermark times are >= 0 (sign bit free)
+
+__device__ __forceinline__ void release_smem() {
+  asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void acquire_smem() {
+  asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void st_rc_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.cluster.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_rc_s32(int* p, int v) {
+  asm volatile("st.relaxed.cluster.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_rc_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.cluster.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_rc_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.cluster.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// an engine's ground truth at a sync (snapshot_stats + BetaEstimator sums), in its own CTA
+struct PipeSnap {
+  long long wpend, enq, fc, fi, fo;
+  int free_b, wr, next, _pad;
+};
+// per-CTA control block (static shared); rank 0's abort / err / counters are the instance's
+struct PipeCtl {
+  unsigned long long wt;  // watermark word (router -> this CTA): time bits | SYNC_BIT
+  int hint[PIPE_WARPS];   // published route counts of this CTA's engines (wake hints)
+  int abort, err;
+  int syncs, polls;       // diagnostics
+  PipeSnap snap[PIPE_WARPS];
+};
+
+// rank 0's dynamic shared memory, per server (n_al = n rounded up to even)
+struct PipeArrays {
+  unsigned long long* done;  // engine -> router: the last sync word it reached
+  long long* rps;            // Σ prompt routed (router)
+  int *cnt, *cnt_pub, *taken;  // routed / published / taken by the engine
+  int* ring;                 // [n][PIPE_RING] routed arrival ids
+  __device__ PipeArrays(long long* b, int n_al) {
+    done = (unsigned long long*)b;
+    rps = b + n_al;
+    int* ib = (int*)(b + 2 * n_al);
+    cnt = ib; cnt_pub = ib + n_al; taken = ib + 2 * n_al;
+    ring = ib + 4 * n_al;
+  }
+};
+__host__ __device__ constexpr long long pipe_array_bytes(int n) {
+  return 8LL * 2 * ((n + 1) & ~1) + 4LL * 4 * ((n + 1) & ~1) + 4LL * PIPE_RING * n;
+}
+
+// the routing warp; VPL view entries per lane (server q = lane + 32 j)
+template <int BAL, int VPL>
+__device__ void pipe_router(const ssb_instance& I, const Cfg& cfg, const double* __restrict__ arr,
+                            const int* __restrict__ prm, PipeArrays A, PipeCtl& C, int G, int publish_every) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int lane = lane_id();
+  const int n = I.n_servers;
+  const long long N = I.n_requests;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  const bool est_beta = BAL == SSB_BAL_SAL && isnan(I.beta_fixed);
+  const int route_cap = I.route_cap;
+  const bool cap_pow2 = route_cap > 0 && (route_cap & (route_cap - 1)) == 0;
+  const double inv_cap = cap_pow2 ? __ddiv_rn(1.0, (double)route_cap) : 0.0;
+  const double poll = I.poll_interval_s;
+  Pcg rng;
+  rng.shi = I.pcg_state_hi; rng.slo = I.pcg_state_lo; rng.ihi = I.pcg_inc_hi; rng.ilo = I.pcg_inc_lo;
+  rng.has = 0; rng.buf = 0;
+  unsigned long long* const wt_lane = lane < G ? &cl.map_shared_rank(&C, lane)->wt : nullptr;
+  // the polled BalancerView (balancers.py:29-64) in registers, and where each server's snapshot lives
+  long long vq[VPL], vf[VPL];
+  int vif[VPL];
+  const PipeSnap* snp[VPL];
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    vq[j] = 0; vf[j] = (long long)cfg.pool * cfg.bs; vif[j] = 0;
+    const int e = lane + 32 * j + 1;  // its engine's cluster warp
+    snp[j] = lane + 32 * j < n ? &cl.map_shared_rank(&C, e / PIPE_WARPS)->snap[e % PIPE_WARPS] : nullptr;
+  }
+  double beta = isnan(I.beta_fixed) ? I.beta_prior : I.beta_fixed;
+  double last_poll = 0.0;  // the refresh at 0.0 (cluster.py:122) sees the empty engines: the init above
+  int synced = 1;
+  int rr_next = 0;
+  // route log: lane i holds the server / prompt of arrival klog + i
+  int slog = 0, plog = 0, nlog = 0;
+  int klog = 0, k = 0, k_pub = 0;
+
+  auto flush = [&]() {  // ring appends, route counters, wake hints for the logged routes
+    if (nlog == 0) return;
+    const bool valid = lane < nlog;
+    const int s = valid ? slog : -1;
+    const unsigned grp = __match_any_sync(FULL, s);
+    const int leader = __ffs(grp) - 1;
+    const int before = __popc(grp & lanemask_lt());
+    const int gsz = __popc(grp);
+    const int base = valid ? A.cnt[s] : 0;
+    // flow control: the engine has taken everything published (base) up to the ring size
+    while (__any_sync(FULL, valid && base + gsz - *(volatile int*)&A.taken[s] > PIPE_RING)) __nanosleep(64);
+    if (valid) {
+      A.ring[s * PIPE_RING + ((base + before) & (PIPE_RING - 1))] = klog + lane;
+      if (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) atomicAdd((unsigned long long*)&A.rps[s], (unsigned long long)(long long)plog);
+    }
+    __syncwarp();
+    release_smem();  // ring slots before their count
+    if (valid && lane == leader) {
+      A.cnt[s] = base + gsz;
+      *(volatile int*)&A.cnt_pub[s] = base + gsz;
+      const int e = s + 1;
+      st_rc_s32(&cl.map_shared_rank(&C, e / PIPE_WARPS)->hint[e % PIPE_WARPS], base + gsz);
+    }
+    __syncwarp();
+    klog += nlog;
+    nlog = 0;
+  };
+  auto publish = [&](unsigned long long word) {
+    flush();
+    release_smem();  // published counts (and abort) before the watermark
+    if (wt_lane) st_rc_u64(wt_lane, word);
+    __syncwarp();
+    k_pub = k;
+  };
+  // every engine to time t (wt = t with the sync bit), then their snapshots are readable
+  auto sync = [&](double t) -> bool {
+    const unsigned long long word = (unsigned long long)__double_as_longlong(t) | SYNC_BIT;
+    publish(word);
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+        if (lane + 32 * j < n) ok &= *(volatile unsigned long long*)&A.done[lane + 32 * j] == word;
+    } while (!__all_sync(FULL, ok));
+    acquire_smem();
+    if (lane == 0) C.syncs += 1;
+    if (*(volatile int*)&C.err) return false;
+    if (est_beta) {  // on_finish sums of every engine (balancers.py:81-100) folded at the sync
+      long long fc = 0, fi = 0, fo = 0;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+        if (snp[j]) { fc += ld_rc_s64(&snp[j]->fc); fi += ld_rc_s64(&snp[j]->fi); fo += ld_rc_s64(&snp[j]->fo); }
+      fc = warp_sum_ll(fc); fi = warp_sum_ll(fi); fo = warp_sum_ll(fo);
+      beta = fc == 0 ? I.beta_prior : __ddiv_rn((double)(fi + fo), (double)fo);
+    }
+    return true;
+  };
+  auto refresh = [&]() {  // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+      if (snp[j]) {
+        const int q = lane + 32 * j;
+        const long long wp = ld_rc_s64(&snp[j]->wpend), en = ld_rc_s64(&snp[j]->enq);
+        const int fb = ld_rc_s32(&snp[j]->free_b), wr = ld_rc_s32(&snp[j]->wr), nx = ld_rc_s32(&snp[j]->next);
+        vq[j] = wp + (A.rps[q] - en);
+        vf[j] = (long long)fb * cfg.bs;
+        vif[j] = wr + (A.cnt[q] - nx);
+      }
+  };
+
+  // arrival times / prompts 32 at a time, the next 32 in flight (lane i holds c0 + i)
+  int c0 = 0;
+  double c_t = lane < N ? arr[lane] : 0.0, n_t = 0.0;
+  int c_pr = lane < N ? prm[lane] : 0, n_pr = 0;
+  if (32 + lane < N) { n_t = arr[32 + lane]; n_pr = prm[32 + lane]; }
+  double t_prev = __shfl_sync(FULL, c_t, 0);
+  bool aborted = false;
+  while (k < N) {
+    if (k >= c0 + 32) {
+      c0 += 32;
+      c_t = n_t; c_pr = n_pr;
+      const long long kk = (long long)c0 + 32 + lane;
+      if (kk < N) { n_t = arr[kk]; n_pr = prm[kk]; }
+    }
+    const double t = __shfl_sync(FULL, c_t, k - c0);
+    const int pr = __shfl_sync(FULL, c_pr, k - c0);
+    synced = t == t_prev ? synced : 0;  // equal times need no sync (no simulated time passes)
+    t_prev = t;
+    int s = 0;
+    if constexpr (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) {
+      if (__dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
+        if (!synced) {
+          if (!sync(t)) { aborted = true; break; }
+          synced = 1;
+        }
+        refresh();
+        last_poll = t;
+        if (lane == 0) C.polls += 1;
+      }
+    }
+    if constexpr (BAL == SSB_BAL_RR) {  // balancers.py:132-142
+      s = rr_next;
+      rr_next = rr_next + 1 == n ? 0 : rr_next + 1;
+    } else if constexpr (BAL == SSB_BAL_RANDOM) {  // :145-153
+      s = rng.integers(n);
+    } else if constexpr (BAL == SSB_BAL_P2C) {  // :156-176, the polled in_flight only
+      if (n > 1) {
+        const int i = rng.integers(n);
+        int j2 = rng.integers(n - 1);
+        if (j2 >= i) j2 += 1;
+        int a = vif[0], b = vif[0];
+#pragma unroll
+        for (int j = 1; j < VPL; ++j) { if ((i >> 5) == j) a = vif[j]; if ((j2 >> 5) == j) b = vif[j]; }
+        a = __shfl_sync(FULL, a, i & 31);
+        b = __shfl_sync(FULL, b, j2 & 31);
+        s = b < a ? j2 : i;
+      }
+    } else {  // SAL (:179-216)
+      // fast path (see k_cluster): one 64-bit warp minimum over (queued+prompt) << 13 |
+      // server << 1 | constrained; an unconstrained winner is the argmin for every beta
+      bool fast = false;
+      if (cap_pow2 && beta > 0.0 && pr > 0) {
+        unsigned long long kx = ~0ULL;
+        bool big = false;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const int q = lane + 32 * j;
+          if (q < n) {
+            const unsigned long long X = (unsigned long long)(vq[j] + pr);
+            big |= X >= (1ULL << 51);
+            const unsigned long long key = (X << 13) | ((unsigned)q << 1) | (unsigned)(vf[j] < pr);
+            kx = key < kx ? key : kx;
+          }
+        }
+        if (!__any_sync(FULL, big)) {
+          const unsigned long long m = warp_min_u64(kx);
+          if (!(m & 1ULL)) { s = (int)((m >> 1) & 0xfffULL); fast = true; }
+          else if (est_beta && !synced) {  // a constrained server leads: beta decides
+            if (!sync(t)) { aborted = true; break; }
+            synced = 1;
+            continue;  // route arrival k again with the synced beta
+          }
+        }
+      }
+      if (!fast) {
+        unsigned long long kl = ~0ULL, ku = ~0ULL, kc = ~0ULL;
+        int sl = 0x7fffffff, su = 0x7fffffff, sc = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const int q = lane + 32 * j;
+          if (q < n) {
+            const double que = cap_pow2 ? __dmul_rn((double)(vq[j] + pr), inv_cap)
+                                        : __ddiv_rn((double)(vq[j] + pr), (double)route_cap);
+            const double mem = __dmul_rn(beta, (double)((long long)pr - vf[j]));
+            const double load = que > mem ? que : mem;  // sal_load (balancers.py:103-112)
+            const unsigned long long k1 = dkey(load), kq = dkey(que);
+            if (k1 < kl) { kl = k1; sl = q; }  // q ascending: ties keep the lower server
+            if (vf[j] < pr) { if (kq < kc) { kc = kq; sc = q; } }
+            else if (kq < ku) { ku = kq; su = q; }
+          }
+        }
+        if (est_beta && !synced) {  // beta-independent argmin? (see k_cluster)
+          const unsigned long long mc = warp_min_u64(kc);
+          if (mc != ~0ULL) {
+            const unsigned long long mu = warp_min_u64(ku);
+            const int iu = mu == ~0ULL ? 0x7fffffff : (int)__reduce_min_sync(FULL, ku == mu ? (unsigned)su : 0x7fffffffu);
+            const int ic = (int)__reduce_min_sync(FULL, kc == mc ? (unsigned)sc : 0x7fffffffu);
+            const bool indep = mu != ~0ULL && (mu < mc || (mu == mc && iu < ic));
+            if (!indep) {
+              if (!sync(t)) { aborted = true; break; }
+              synced = 1;
+              continue;
+            }
+          }
+        }
+        const unsigned long long ml = warp_min_u64(kl);
+        s = (int)__reduce_min_sync(FULL, kl == ml ? (unsigned)sl : 0x7fffffffu);
+      }
+      // note_routed (balancers.py:59-64) on the owner lane
+      if (lane == (s & 31)) {
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if ((s >> 5) == j) {
+            vq[j] += pr;
+            const long long f = vf[j] - pr;
+            vf[j] = f > 0 ? f : 0;
+            vif[j] += 1;
+          }
+      }
+    }
+    if (lane == nlog) { slog = s; plog = pr; }
+    nlog += 1;
+    k += 1;
+    if (nlog == 32) flush();
+    if (k - k_pub >= publish_every && k < N) {
+      const double tn = k < c0 + 32 ? __shfl_sync(FULL, c_t, k - c0) : __shfl_sync(FULL, n_t, k - c0 - 32);
+      publish((unsigned long long)__double_as_longlong(tn));
+    }
+  }
+  if (aborted) {
+    if (lane == 0) C.abort = 1;
+    publish((unsigned long long)__double_as_longlong(INF) | SYNC_BIT);  // wake everyone
+    return;
+  }
+  sync(INF);  // drain: every engine to the end
+}
+
+template <int POL>
+__device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst, const int* __restrict__ order,
+                                          ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
+                                          unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
+                                          int64_t* ev_count, long long* smem_ll, PipeCtl& C, int publish_every) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int idx = order[blockIdx.x / G];
+  const ssb_instance I = inst[idx];
+  const int n = I.n_servers;
+  const long long N = I.n_requests;
+  const int n_al = (n + 1) & ~1;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int gw = rank * PIPE_WARPS + warp;
+  const int s = gw - 1;  // this warp's server (gw 0 routes)
+  PipeCtl& C0 = rank == 0 ? C : *cl.map_shared_rank(&C, 0);
+  PipeArrays A(rank == 0 ? smem_ll : cl.map_shared_rank(smem_ll, 0), n_al);
+  int* const tab = (int*)((unsigned char*)smem_ll + align_up(pipe_array_bytes(n), 16)) + warp * SM_COLS * RS;
+  Cfg cfg = make_cfg(I);
+  cfg.policy = POL;
+  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
+  ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+
+  // ---- init: control blocks, rank 0's counters, records, engines ----
+  if (threadIdx.x == 0) {
+    C.wt = 0ULL;  // +0.0, no sync: nothing routed
+    C.abort = C.err = C.syncs = C.polls = 0;
+  }
+  if (threadIdx.x < PIPE_WARPS) C.hint[threadIdx.x] = 0;
+  if (rank == 0)
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      A.done[q] = 0ULL;
+      A.rps[q] = 0;
+      A.cnt[q] = A.cnt_pub[q] = A.taken[q] = 0;
+    }
+  {
+    Eng E;
+    bind_engine(E, I, cfg, scratch, 0, L, tr, rec, evb, ev_cap);
+    clear_records(E, N, rank * blockDim.x + threadIdx.x, G * blockDim.x);
+  }
+  Eng E;
+  const bool engine = s >= 0 && s < n;
+  if (engine) {
+    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab);
+    init_srv(E.st, cfg);
+    if (POL == SSB_POLICY_TRAIL_PLUS) E.trail_init();
+    fill_events(E, lane, 32);
+    if (lane == 0) {  // the snapshot of the empty engine: a refresh before the first sync reads it
+      PipeSnap& sn = C.snap[warp];
+      sn.wpend = sn.enq = sn.fc = sn.fi = sn.fo = 0;
+      sn.free_b = cfg.pool;
+      sn.wr = sn.next = sn._pad = 0;
+    }
+  }
+  cl.sync();
+
+  if (gw == 0) {
+    const double* arr = instance_arrivals(I, L, tr, scratch);  // already divided by qps_factor
+    const int* prm = tr.prompt + I.trace_offset;
+    const bool v2 = n <= 64;
+    switch (I.balancer) {
+      case SSB_BAL_RR: pipe_router<SSB_BAL_RR, 1>(I, cfg, arr, prm, A, C, G, 32); break;
+      case SSB_BAL_RANDOM: pipe_router<SSB_BAL_RANDOM, 1>(I, cfg, arr, prm, A, C, G, 32); break;
+      case SSB_BAL_P2C:
+        if (v2) pipe_router<SSB_BAL_P2C, 2>(I, cfg, arr, prm, A, C, G, publish_every);
+        else pipe_router<SSB_BAL_P2C, 4>(I, cfg, arr, prm, A, C, G, publish_every);
+        break;
+      default:
+        if (v2) pipe_router<SSB_BAL_SAL, 2>(I, cfg, arr, prm, A, C, G, publish_every);
+        else pipe_router<SSB_BAL_SAL, 4>(I, cfg, arr, prm, A, C, G, publish_every);
+        break;
+    }
+  } else if (engine) {
+    // ---- engine: take the new routes, advance to every watermark that lets it progress ----
+    E.init_modes();
+    unsigned long long seen = 0ULL;
+    int seen_hint = 0, taken = 0;
+    double nb_lb = INF;  // lower bound of its next boundary: idle with nothing routed
+    bool reported = false;
+    volatile PipeCtl& V = C;
+    const int* ring = A.ring + s * PIPE_RING;
+    while (true) {
+      unsigned long long w;
+      while (true) {
+        w = V.wt;
+        const int h = V.hint[warp];
+        if (w != seen || h != seen_hint) {
+          const double wt = __longlong_as_double((long long)(w & ~SYNC_BIT));
+          if ((w & SYNC_BIT) || nb_lb < wt || h != seen_hint) break;
+          seen = w;  // nothing to do before this watermark
+        } else {
+          __nanosleep(32);
+        }
+      }
+      seen = w;
+      acquire_smem();
+      // take the published routes into the engine's own route list (global, rl)
+      const int cp = ld_rc_s32(&A.cnt_pub[s]);
+      if (cp > taken) {
+        int dep = 0;
+        for (int b = taken; b < cp; b += 32) {
+          const int i = b + lane;
+          if (i < cp) {
+            const int v = ld_rc_s32(&ring[i & (PIPE_RING - 1)]);
+            E.p.rl[i] = v;
+            dep |= v;
+          }
+        }
+        taken = cp;
+        // the reported count depends on the loaded ids: the slots are read before the router reuses them
+        dep = __reduce_or_sync(FULL, dep);
+        if (lane == 0) st_rc_s32(&A.taken[s], dep == -1 ? 0 : cp);
+        __syncwarp();
+      }
+      seen_hint = cp;
+      const bool sync = (w & SYNC_BIT) != 0;
+      const double wt = __longlong_as_double((long long)(w & ~SYNC_BIT));
+      if (sync && ld_rc_s32(&C0.abort)) {
+        if (lane == 0) st_rc_u64(&A.done[s], w);
+        break;
+      }
+      E.advance_loop(wt, taken);
+      if (E.st.status && !reported) {
+        reported = true;
+        if (lane == 0) st_rc_s32(&C0.err, E.st.status);
+      }
+      if (E.has_work()) {
+        nb_lb = E.st.clock;
+      } else {
+        const double na = E.next_arrival(taken);
+        nb_lb = na > E.st.clock ? na : E.st.clock;
+      }
+      if (sync) {
+        if (lane == 0) {  // the ground-truth snapshot at wt (snapshot_stats, cluster.py:50-59)
+          PipeSnap& sn = C.snap[warp];
+          sn.wpend = E.st.wpend_sum;
+          sn.enq = E.st.enq_prompt_sum;
+          sn.fc = E.st.fin_cnt;
+          sn.fi = E.st.fin_in;
+          sn.fo = E.st.fin_out;
+          sn.free_b = E.st.free_blocks;
+          sn.wr = E.st.W + E.st.R;
+          sn.next = E.st.next_arr;
+        }
+        __syncwarp();
+        release_smem();
+        if (lane == 0) st_rc_u64(&A.done[s], w);
+        if (!(wt < INF)) break;
+      }
+    }
+    E.drop_regs();
+    if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
+  }
+  cl.sync();  // every engine's state is in memory; rank 0's shared memory outlives its readers
+
+  // ---------------- per-instance stats ----------------
+  if (rank == 0 && threadIdx.x == 0) {
+    ssb_stats out;
+    memset(&out, 0, sizeof(out));
+    unsigned long long h = FNV_OFF;
+    int status = C.err;
+    long long evn = 0;
+    for (int q = 0; q < n; ++q) {
+      const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)q * L.total + L.srv);
+      out.iterations += sv->iterations;
+      out.request_steps += sv->rsteps;
+      out.batch_tokens += sv->btokens;
+      out.dispatches += sv->dispatches;
+      out.preempts += sv->preempts;
+      out.parks += sv->parks;
+      out.finished += sv->finished;
+      if (sv->peak > out.peak_batch_tokens) out.peak_batch_tokens = sv->peak;
+      h ^= sv->digest; h *= FNV_PRIME;
+      if (!status && sv->status) status = sv->status;
+      if (!status && (sv->W != 0 || sv->R != 0)) status = SSB_E_INVARIANT;
+      evn += sv->ev_n;
+    }
+    if (!status && out.finished != N) status = SSB_E_INVARIANT;  // cluster.py:159-161
+    out.digest = h;
+    out.status = status;
+#ifdef SSB_PIPE_PROBE
+    out._pad = C.syncs;            // diagnostics: engine syncs (routing epochs)
+    out.device_cycles = C.polls;   //              view refreshes
+#endif
+    stats[idx] = out;
+    if (ev_count) ev_count[idx] = evn;
+  }
+}
+
+__global__ void __launch_bounds__(32 * PIPE_WARPS, 1)
+k_cluster_pipe(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr, ssb_records rec,
+               ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
+               int64_t* ev_count, int publish_every) {
+  extern __shared__ long long smem_ll[];
+  __shared__ PipeCtl C;
+  const int G = (int)cg::this_cluster().num_blocks();
+  switch (inst[order[blockIdx.x / G]].engine.policy) {
+    case SSB_POLICY_FCFS: pipe_body<SSB_POLICY_FCFS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
+    case SSB_POLICY_NOPREEMPT: pipe_body<SSB_POLICY_NOPREEMPT>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
+    case SSB_POLICY_TRAIL_PLUS: pipe_body<SSB_POLICY_TRAIL_PLUS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
+    default: pipe_body<SSB_POLICY_LARRY>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
+  }
+}
+
 // per-engine counters: a cluster's servers from the per-server state k_cluster leaves in
 // the scratch buffer after every advance; a single-server instance from its ssb_stats
 // (k_engines keeps no per-engine copy: one more store of the engine state at the end of
@@ -1106,7 +1645,36 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     k_scale_arrivals<<<(unsigned)std::min(n_inst, 8 * sms), 256, 0, stream>>>(d_inst, n_inst, trace, scratch);
     if (cudaGetLastError() != cudaSuccess) return SSB_E_CUDA;
   }
-  if (!multis.empty()) {
+  bool multis_done = multis.empty();
+  if (!multis_done && max_servers <= PIPE_MAX_SERVERS && getenv("SSB_CLUSTER_CLASSIC") == nullptr) {
+    // pipelined: one cluster of G CTAs x 8 warps per instance, a routing warp + one warp per
+    // replica (G = 9 for 64 replicas: a non-portable cluster size)
+    const int G = (max_servers + 1 + PIPE_WARPS - 1) / PIPE_WARPS;
+    int publish_every = 8;
+    if (const char* e = getenv("SSB_PIPE_PUBLISH")) publish_every = std::max(1, atoi(e));  // experiments
+    const size_t smc = align_up(pipe_array_bytes(max_servers), 16) + sizeof(int) * SM_COLS * RS * PIPE_WARPS;
+    cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+    if (G > 8) cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(multis.size() * G));
+    lc.blockDim = dim3(32 * PIPE_WARPS);
+    lc.dynamicSmemBytes = smc;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, k_cluster_pipe, (const ssb_instance*)d_inst, (const int*)(d_hdr + off_multi), trace,
+                           records, d_stats, scratch, d_events, (long long)event_cap, (int64_t*)d_event_count,
+                           publish_every) == cudaSuccess)
+      multis_done = true;
+    else
+      cudaGetLastError();  // e.g. the cluster size does not fit: the classic kernel below
+  }
+  if (!multis_done) {
     // one cluster of G CTAs x nw warps per instance: enough warps for one replica each (<= 64)
     const int nw = std::min(CLUSTER_MAX_WARPS, max_servers);
     const int G = std::min(CLUSTER_MAX_CTAS, (max_servers + nw - 1) / nw);
