@@ -882,9 +882,14 @@ __global__ void __launch_bounds__(32 * CLUSTER_MAX_WARPS, 1) k_cluster(const ssb
 //     into rank 0.
 constexpr int PIPE_WARPS = 8;
 constexpr int PIPE_MAX_CTAS = 16;  // non-portable cluster size (cudaFuncAttributeNonPortableClusterSizeAllowed)
-constexpr int PIPE_MAX_SERVERS = PIPE_WARPS * PIPE_MAX_CTAS - 1;
+constexpr int PIPE_MAX_SERVERS = PIPE_WARPS * (PIPE_MAX_CTAS - 1);
 constexpr int PIPE_RING = 128;     // routed ids in flight per server (>= 32: one route-log flush)
 constexpr unsigned long long SYNC_BIT = 0x8000000000000000ULL;  // watermark times are >= 0 (sign bit free)
+
+// cluster warp of server s: rank 0 is the routing warp's alone (its SM's issue slots and
+// shared-memory port serve the serial routing chain), the servers take every warp of ranks 1..
+__host__ __device__ constexpr int pipe_gw(int s) { return s + PIPE_WARPS; }
+__device__ __forceinline__ int pipe_server(int gw) { return gw >= PIPE_WARPS ? gw - PIPE_WARPS : -1; }
 
 __device__ __forceinline__ void release_smem() {
   asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
@@ -903,6 +908,11 @@ __device__ __forceinline__ int ld_rc_s32(const int* p) {
   asm volatile("ld.relaxed.cluster.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_rc_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.cluster.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ long long ld_rc_s64(const long long* p) {
   long long v;
   asm volatile("ld.relaxed.cluster.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -913,7 +923,14 @@ __device__ __forceinline__ long long ld_rc_s64(const long long* p) {
 struct PipeSnap {
   long long wpend, enq, fc, fi, fo;
   int free_b, wr, next, _pad;
+  unsigned long long done;  // the last sync word the engine reached (read by the router over DSMEM)
 };
+#ifdef SSB_PIPE_TIMELINE
+// sync timeline of the first instance (tools/probe_sync.py): per sync, the router's publish and
+// all-done %globaltimer ns, then per server (wake ns, done ns, iterations run in that wake)
+constexpr int SYNC_TL_MAX = 4096, SYNC_TL_W = 2 + 3 * 128;
+__device__ unsigned long long g_sync_tl[SYNC_TL_MAX * SYNC_TL_W];
+#endif
 // per-CTA control block (static shared); rank 0's abort / err / counters are the instance's
 struct PipeCtl {
   unsigned long long wt;  // watermark word (router -> this CTA): time bits | SYNC_BIT
@@ -921,6 +938,9 @@ struct PipeCtl {
   int abort, err;
   int syncs, polls;       // diagnostics
   PipeSnap snap[PIPE_WARPS];
+#ifdef SSB_PIPE_PROBE
+  unsigned long long p_wait, p_route, p_flush, p_busy_sum, p_busy_max, p_wakes, p_iters_max, p_take, p_arr, p_pub, p_sync, p_chunk;
+#endif
 };
 
 // rank 0's dynamic shared memory, per server (n_al = n rounded up to even)
@@ -941,140 +961,208 @@ __host__ __device__ constexpr long long pipe_array_bytes(int n) {
   return 8LL * 2 * ((n + 1) & ~1) + 4LL * 4 * ((n + 1) & ~1) + 4LL * PIPE_RING * n;
 }
 
-// the routing warp; VPL view entries per lane (server q = lane + 32 j)
+// the routing warp. Plain locals and force-inlined helpers that take them by reference
+// (a struct or lambdas holding the view put it in local memory: measured, the fast path then
+// paid local loads per arrival)
+struct PipeLog {  // route log: lane i holds the server / prompt of arrival klog + i
+  int slog, plog, nlog, klog;
+};
+// publish: append the logged routes to their rings, ONE release (MEMBAR.ALL.CTA: it waits for
+// the warp's outstanding stores, so a publish costs one), then the wake hints (the new counts)
+// and the watermark word. The log holds at most 32 routes (publish_every <= 32), and it is
+// only flushed here, so every ring slot the flow control waits on was hinted before.
+template <int BAL>
+__device__ __forceinline__ void pipe_publish(PipeLog& g, PipeArrays& A, PipeCtl& C, int lane,
+                                             unsigned long long* wt_lane, unsigned long long word) {
+#ifdef SSB_PIPE_PROBE
+  const long long pf0 = clock64();
+#endif
+  cg::cluster_group cl = cg::this_cluster();
+  const bool valid = lane < g.nlog;
+  const int s = valid ? g.slog : -1;
+  const unsigned grp = __match_any_sync(FULL, s);
+  const int leader = __ffs(grp) - 1;
+  const int before = __popc(grp & lanemask_lt());
+  const int gsz = __popc(grp);
+  int base = 0;
+  if (g.nlog) {
+    base = valid ? A.cnt[s] : 0;
+    // flow control: the engine has taken everything published (base) up to the ring size
+    while (__any_sync(FULL, valid && base + gsz - *(volatile int*)&A.taken[s] > PIPE_RING)) __nanosleep(64);
+    if (valid) {
+      A.ring[s * PIPE_RING + ((base + before) & (PIPE_RING - 1))] = g.klog + lane;
+      if (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) atomicAdd((unsigned long long*)&A.rps[s], (unsigned long long)(long long)g.plog);
+      if (lane == leader) A.cnt[s] = base + gsz;
+    }
+    __syncwarp();
+  }
+  release_smem();  // ring slots (and abort) before their counts and the watermark
+  if (valid && lane == leader) {
+    const int e = pipe_gw(s);
+    st_rc_s32(&cl.map_shared_rank(&C, e / PIPE_WARPS)->hint[e % PIPE_WARPS], base + gsz);
+  }
+  if (wt_lane) st_rc_u64(wt_lane, word);
+  __syncwarp();
+  g.klog += g.nlog;
+  g.nlog = 0;
+#ifdef SSB_PIPE_PROBE
+  if (lane == 0) C.p_flush += clock64() - pf0;
+#endif
+}
+
 template <int BAL, int VPL>
-__device__ void pipe_router(const ssb_instance& I, const Cfg& cfg, const double* __restrict__ arr,
-                            const int* __restrict__ prm, PipeArrays A, PipeCtl& C, int G, int publish_every) {
+__device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cfg, const double* __restrict__ arr,
+                                            const int* __restrict__ prm, PipeArrays A, PipeCtl& C, int G,
+                                            int publish_every) {
   cg::cluster_group cl = cg::this_cluster();
   const int lane = lane_id();
   const int n = I.n_servers;
   const long long N = I.n_requests;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
   const bool est_beta = BAL == SSB_BAL_SAL && isnan(I.beta_fixed);
+  const double beta_prior = I.beta_prior;
   const int route_cap = I.route_cap;
   const bool cap_pow2 = route_cap > 0 && (route_cap & (route_cap - 1)) == 0;
   const double inv_cap = cap_pow2 ? __ddiv_rn(1.0, (double)route_cap) : 0.0;
   const double poll = I.poll_interval_s;
+  const int bs = cfg.bs;
   Pcg rng;
   rng.shi = I.pcg_state_hi; rng.slo = I.pcg_state_lo; rng.ihi = I.pcg_inc_hi; rng.ilo = I.pcg_inc_lo;
   rng.has = 0; rng.buf = 0;
   unsigned long long* const wt_lane = lane < G ? &cl.map_shared_rank(&C, lane)->wt : nullptr;
-  // the polled BalancerView (balancers.py:29-64) in registers, and where each server's snapshot lives
+  // the polled BalancerView (balancers.py:29-64) in registers: queued tokens also as the SAL
+  // key key0 = queued << 13 | server << 1 (the argmin order of queued+prompt with the lowest
+  // server among ties; ~0 for lanes past n), free memory, in-flight; where each snapshot lives
+  unsigned long long key0[VPL];
   long long vq[VPL], vf[VPL];
   int vif[VPL];
   const PipeSnap* snp[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
-    vq[j] = 0; vf[j] = (long long)cfg.pool * cfg.bs; vif[j] = 0;
-    const int e = lane + 32 * j + 1;  // its engine's cluster warp
-    snp[j] = lane + 32 * j < n ? &cl.map_shared_rank(&C, e / PIPE_WARPS)->snap[e % PIPE_WARPS] : nullptr;
+    const int q = lane + 32 * j;
+    key0[j] = q < n ? (unsigned long long)q << 1 : ~0ULL;
+    vq[j] = 0; vf[j] = (long long)cfg.pool * bs; vif[j] = 0;
+    snp[j] = q < n ? &cl.map_shared_rank(&C, pipe_gw(q) / PIPE_WARPS)->snap[pipe_gw(q) % PIPE_WARPS] : nullptr;
   }
-  double beta = isnan(I.beta_fixed) ? I.beta_prior : I.beta_fixed;
+  bool anybig = false;  // some queued >= 2^50: the integer key would not be exact (warp-uniform)
+  double beta = isnan(I.beta_fixed) ? beta_prior : I.beta_fixed;
+  PipeLog g;
+  g.slog = g.plog = g.nlog = g.klog = 0;
+  int k = 0, k_pub = 0;
   double last_poll = 0.0;  // the refresh at 0.0 (cluster.py:122) sees the empty engines: the init above
   int synced = 1;
   int rr_next = 0;
-  // route log: lane i holds the server / prompt of arrival klog + i
-  int slog = 0, plog = 0, nlog = 0;
-  int klog = 0, k = 0, k_pub = 0;
-
-  auto flush = [&]() {  // ring appends, route counters, wake hints for the logged routes
-    if (nlog == 0) return;
-    const bool valid = lane < nlog;
-    const int s = valid ? slog : -1;
-    const unsigned grp = __match_any_sync(FULL, s);
-    const int leader = __ffs(grp) - 1;
-    const int before = __popc(grp & lanemask_lt());
-    const int gsz = __popc(grp);
-    const int base = valid ? A.cnt[s] : 0;
-    // flow control: the engine has taken everything published (base) up to the ring size
-    while (__any_sync(FULL, valid && base + gsz - *(volatile int*)&A.taken[s] > PIPE_RING)) __nanosleep(64);
-    if (valid) {
-      A.ring[s * PIPE_RING + ((base + before) & (PIPE_RING - 1))] = klog + lane;
-      if (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) atomicAdd((unsigned long long*)&A.rps[s], (unsigned long long)(long long)plog);
-    }
-    __syncwarp();
-    release_smem();  // ring slots before their count
-    if (valid && lane == leader) {
-      A.cnt[s] = base + gsz;
-      *(volatile int*)&A.cnt_pub[s] = base + gsz;
-      const int e = s + 1;
-      st_rc_s32(&cl.map_shared_rank(&C, e / PIPE_WARPS)->hint[e % PIPE_WARPS], base + gsz);
-    }
-    __syncwarp();
-    klog += nlog;
-    nlog = 0;
-  };
-  auto publish = [&](unsigned long long word) {
-    flush();
-    release_smem();  // published counts (and abort) before the watermark
-    if (wt_lane) st_rc_u64(wt_lane, word);
-    __syncwarp();
-    k_pub = k;
-  };
-  // every engine to time t (wt = t with the sync bit), then their snapshots are readable
-  auto sync = [&](double t) -> bool {
-    const unsigned long long word = (unsigned long long)__double_as_longlong(t) | SYNC_BIT;
-    publish(word);
-    bool ok;
-    do {
-      ok = true;
-#pragma unroll
-      for (int j = 0; j < VPL; ++j)
-        if (lane + 32 * j < n) ok &= *(volatile unsigned long long*)&A.done[lane + 32 * j] == word;
-    } while (!__all_sync(FULL, ok));
-    acquire_smem();
-    if (lane == 0) C.syncs += 1;
-    if (*(volatile int*)&C.err) return false;
-    if (est_beta) {  // on_finish sums of every engine (balancers.py:81-100) folded at the sync
-      long long fc = 0, fi = 0, fo = 0;
-#pragma unroll
-      for (int j = 0; j < VPL; ++j)
-        if (snp[j]) { fc += ld_rc_s64(&snp[j]->fc); fi += ld_rc_s64(&snp[j]->fi); fo += ld_rc_s64(&snp[j]->fo); }
-      fc = warp_sum_ll(fc); fi = warp_sum_ll(fi); fo = warp_sum_ll(fo);
-      beta = fc == 0 ? I.beta_prior : __ddiv_rn((double)(fi + fo), (double)fo);
-    }
-    return true;
-  };
-  auto refresh = [&]() {  // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
-#pragma unroll
-    for (int j = 0; j < VPL; ++j)
-      if (snp[j]) {
-        const int q = lane + 32 * j;
-        const long long wp = ld_rc_s64(&snp[j]->wpend), en = ld_rc_s64(&snp[j]->enq);
-        const int fb = ld_rc_s32(&snp[j]->free_b), wr = ld_rc_s32(&snp[j]->wr), nx = ld_rc_s32(&snp[j]->next);
-        vq[j] = wp + (A.rps[q] - en);
-        vf[j] = (long long)fb * cfg.bs;
-        vif[j] = wr + (A.cnt[q] - nx);
-      }
-  };
-
   // arrival times / prompts 32 at a time, the next 32 in flight (lane i holds c0 + i)
   int c0 = 0;
   double c_t = lane < N ? arr[lane] : 0.0, n_t = 0.0;
   int c_pr = lane < N ? prm[lane] : 0, n_pr = 0;
   if (32 + lane < N) { n_t = arr[32 + lane]; n_pr = prm[32 + lane]; }
-  double t_prev = __shfl_sync(FULL, c_t, 0);
-  bool aborted = false;
-  while (k < N) {
+  // per chunk, as bit masks over its 32 arrivals: the arrival's time equals the previous one's
+  // (no simulated time passes: a sync stays valid), and the arrival is due for a poll refresh
+  // (BalancerView.due, balancers.py:42-43, against the current last_poll)
+  unsigned eq_mask = 0, due_mask = 0;
+  auto chunk_masks = [&](double t_last) {
+    const double up = __shfl_up_sync(FULL, c_t, 1);
+    eq_mask = __ballot_sync(FULL, (lane == 0 ? t_last : up) == c_t);
+    if (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) due_mask = __ballot_sync(FULL, __dsub_rn(c_t, last_poll) >= poll);
+  };
+  chunk_masks(__shfl_sync(FULL, c_t, 0));  // arrival 0: the engines are synced at the start
+  bool aborted = false, need_sync = false;
+  double t_sync = 0.0;
+#ifdef SSB_PIPE_PROBE
+  const long long pr0 = clock64();
+#endif
+  while (true) {
+    if (need_sync) {
+      // the one sync site (a route that reads engine state, or the final drain): every engine
+      // to time t_sync (wt = t_sync with the sync bit), then their snapshots are readable
+      need_sync = false;
+#ifdef SSB_PIPE_PROBE
+      const long long ps0 = clock64();
+#endif
+      const unsigned long long word = (unsigned long long)__double_as_longlong(t_sync) | SYNC_BIT;
+#ifdef SSB_PIPE_TIMELINE
+      const unsigned long long tl0 = globaltimer_ns();
+#endif
+      pipe_publish<BAL>(g, A, C, lane, wt_lane, word);
+      k_pub = k;
+#ifdef SSB_PIPE_PROBE
+      const long long pw0 = clock64();
+#endif
+      bool ok;
+      do {  // each engine's done word in its own CTA, polled over DSMEM (one round trip per pass)
+        ok = true;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (snp[j]) ok &= ld_rc_u64(&snp[j]->done) == word;
+      } while (!__all_sync(FULL, ok));
+      acquire_smem();
+#ifdef SSB_PIPE_PROBE
+      if (lane == 0) C.p_wait += clock64() - pw0;
+#endif
+#ifdef SSB_PIPE_TIMELINE
+      if (lane == 0 && blockIdx.x == 0 && C.syncs < SYNC_TL_MAX) {
+        g_sync_tl[(long long)C.syncs * SYNC_TL_W] = tl0;
+        g_sync_tl[(long long)C.syncs * SYNC_TL_W + 1] = globaltimer_ns();
+      }
+#endif
+      if (lane == 0) C.syncs += 1;
+      if (*(volatile int*)&C.err) { aborted = true; break; }
+      if (est_beta) {  // on_finish sums of every engine (balancers.py:81-100) folded at the sync
+        long long fc = 0, fi = 0, fo = 0;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (snp[j]) { fc += ld_rc_s64(&snp[j]->fc); fi += ld_rc_s64(&snp[j]->fi); fo += ld_rc_s64(&snp[j]->fo); }
+        fc = warp_sum_ll(fc); fi = warp_sum_ll(fi); fo = warp_sum_ll(fo);
+        beta = fc == 0 ? beta_prior : __ddiv_rn((double)(fi + fo), (double)fo);
+      }
+      synced = 1;
+#ifdef SSB_PIPE_PROBE
+      if (lane == 0) C.p_sync += clock64() - ps0;
+#endif
+      if (k >= N) break;
+    }
+    if (k >= N) { t_sync = INF; need_sync = true; continue; }  // drain: every engine to the end
+#ifdef SSB_PIPE_PROBE
+    const long long pc0 = clock64();
+#endif
     if (k >= c0 + 32) {
+      const double t_last = __shfl_sync(FULL, c_t, 31);
       c0 += 32;
       c_t = n_t; c_pr = n_pr;
       const long long kk = (long long)c0 + 32 + lane;
       if (kk < N) { n_t = arr[kk]; n_pr = prm[kk]; }
+      chunk_masks(t_last);
     }
-    const double t = __shfl_sync(FULL, c_t, k - c0);
-    const int pr = __shfl_sync(FULL, c_pr, k - c0);
-    synced = t == t_prev ? synced : 0;  // equal times need no sync (no simulated time passes)
-    t_prev = t;
+#ifdef SSB_PIPE_PROBE
+    const long long pa0 = clock64();
+    if (lane == 0) C.p_chunk += pa0 - pc0;
+#endif
+    const int ik = k - c0;
+    const int pr = __shfl_sync(FULL, c_pr, ik);
+    synced = (eq_mask >> ik) & 1u ? synced : 0;  // equal times need no sync (no simulated time passes)
     int s = 0;
     if constexpr (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) {
-      if (__dsub_rn(t, last_poll) >= poll) {  // BalancerView.due (balancers.py:42-43)
-        if (!synced) {
-          if (!sync(t)) { aborted = true; break; }
-          synced = 1;
-        }
-        refresh();
+      if ((due_mask >> ik) & 1u) {  // BalancerView.due (balancers.py:42-43)
+        const double t = __shfl_sync(FULL, c_t, ik);
+        if (!synced) { need_sync = true; t_sync = t; eq_mask |= 1u << ik; continue; }
+        // ground truth incl. routed-but-unseen inbox (cluster.py:110-120, 50-59)
+        bool big = false;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+          if (snp[j]) {
+            const int q = lane + 32 * j;
+            const long long wp = ld_rc_s64(&snp[j]->wpend), en = ld_rc_s64(&snp[j]->enq);
+            const int fb = ld_rc_s32(&snp[j]->free_b), wr = ld_rc_s32(&snp[j]->wr), nx = ld_rc_s32(&snp[j]->next);
+            vq[j] = wp + (A.rps[q] - en);
+            key0[j] = ((unsigned long long)vq[j] << 13) | ((unsigned)q << 1);
+            big |= vq[j] >= (1LL << 50);
+            vf[j] = (long long)fb * bs;
+            vif[j] = wr + (A.cnt[q] - nx);
+          }
+        anybig = __any_sync(FULL, big);
         last_poll = t;
+        due_mask = __ballot_sync(FULL, __dsub_rn(c_t, last_poll) >= poll);
         if (lane == 0) C.polls += 1;
       }
     }
@@ -1089,37 +1177,33 @@ __device__ void pipe_router(const ssb_instance& I, const Cfg& cfg, const double*
         int j2 = rng.integers(n - 1);
         if (j2 >= i) j2 += 1;
         int a = vif[0], b = vif[0];
+        const unsigned mi = 1u << (i >> 5), mj = 1u << (j2 >> 5);
 #pragma unroll
-        for (int j = 1; j < VPL; ++j) { if ((i >> 5) == j) a = vif[j]; if ((j2 >> 5) == j) b = vif[j]; }
+        for (int j = 1; j < VPL; ++j) { a = (mi >> j) & 1u ? vif[j] : a; b = (mj >> j) & 1u ? vif[j] : b; }
         a = __shfl_sync(FULL, a, i & 31);
         b = __shfl_sync(FULL, b, j2 & 31);
         s = b < a ? j2 : i;
       }
     } else {  // SAL (:179-216)
-      // fast path (see k_cluster): one 64-bit warp minimum over (queued+prompt) << 13 |
-      // server << 1 | constrained; an unconstrained winner is the argmin for every beta
+      // fast path (see k_cluster): a 64-bit warp minimum over queued << 13 | server << 1 |
+      // constrained ((queued + prompt, server) orders as (queued, server): the prompt is
+      // common); an unconstrained winner is the load argmin for every beta
       bool fast = false;
-      if (cap_pow2 && beta > 0.0 && pr > 0) {
-        unsigned long long kx = ~0ULL;
-        bool big = false;
+      if (cap_pow2 && beta > 0.0 && pr > 0 && !anybig) {
+        unsigned long long kx = key0[0] | (unsigned long long)(vf[0] < pr);
 #pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-          const int q = lane + 32 * j;
-          if (q < n) {
-            const unsigned long long X = (unsigned long long)(vq[j] + pr);
-            big |= X >= (1ULL << 51);
-            const unsigned long long key = (X << 13) | ((unsigned)q << 1) | (unsigned)(vf[j] < pr);
-            kx = key < kx ? key : kx;
-          }
+        for (int j = 1; j < VPL; ++j) {
+          const unsigned long long key = key0[j] | (unsigned long long)(vf[j] < pr);
+          kx = key < kx ? key : kx;
         }
-        if (!__any_sync(FULL, big)) {
-          const unsigned long long m = warp_min_u64(kx);
-          if (!(m & 1ULL)) { s = (int)((m >> 1) & 0xfffULL); fast = true; }
-          else if (est_beta && !synced) {  // a constrained server leads: beta decides
-            if (!sync(t)) { aborted = true; break; }
-            synced = 1;
-            continue;  // route arrival k again with the synced beta
-          }
+        const unsigned long long m = warp_min_u64(kx);
+        if (!(m & 1ULL)) {
+          s = (int)((m >> 1) & 0xfffULL);
+          fast = true;
+          anybig = (long long)(m >> 13) + pr >= (1LL << 50);  // the winner's queued after note_routed
+        } else if (est_beta && !synced) {  // a constrained server leads: beta decides
+          need_sync = true; t_sync = __shfl_sync(FULL, c_t, ik); eq_mask |= 1u << ik;
+          continue;  // then route arrival k again
         }
       }
       if (!fast) {
@@ -1146,43 +1230,55 @@ __device__ void pipe_router(const ssb_instance& I, const Cfg& cfg, const double*
             const int iu = mu == ~0ULL ? 0x7fffffff : (int)__reduce_min_sync(FULL, ku == mu ? (unsigned)su : 0x7fffffffu);
             const int ic = (int)__reduce_min_sync(FULL, kc == mc ? (unsigned)sc : 0x7fffffffu);
             const bool indep = mu != ~0ULL && (mu < mc || (mu == mc && iu < ic));
-            if (!indep) {
-              if (!sync(t)) { aborted = true; break; }
-              synced = 1;
-              continue;
-            }
+            if (!indep) { need_sync = true; t_sync = __shfl_sync(FULL, c_t, ik); eq_mask |= 1u << ik; continue; }
           }
         }
         const unsigned long long ml = warp_min_u64(kl);
         s = (int)__reduce_min_sync(FULL, kl == ml ? (unsigned)sl : 0x7fffffffu);
-      }
-      // note_routed (balancers.py:59-64) on the owner lane
-      if (lane == (s & 31)) {
+        const unsigned own = lane == (s & 31) ? 1u << (s >> 5) : 0u;
+        bool b = false;
 #pragma unroll
-        for (int j = 0; j < VPL; ++j)
-          if ((s >> 5) == j) {
-            vq[j] += pr;
-            const long long f = vf[j] - pr;
-            vf[j] = f > 0 ? f : 0;
-            vif[j] += 1;
-          }
+        for (int j = 0; j < VPL; ++j) b |= ((own >> j) & 1u) && vq[j] + pr >= (1LL << 50);
+        anybig = __any_sync(FULL, b) || anybig;
+      }
+      // note_routed (balancers.py:59-64) on the owner lane: per-element selects on a bit mask,
+      // so that no dynamically indexed access puts the view in local memory
+      const unsigned own = lane == (s & 31) ? 1u << (s >> 5) : 0u;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const bool o = (own >> j) & 1u;
+        key0[j] = o ? key0[j] + ((unsigned long long)pr << 13) : key0[j];  // exact while queued < 2^50 (else anybig)
+        vq[j] = o ? vq[j] + pr : vq[j];
+        const long long f = vf[j] - pr;
+        vf[j] = o ? (f > 0 ? f : 0) : vf[j];
+        vif[j] = o ? vif[j] + 1 : vif[j];
       }
     }
-    if (lane == nlog) { slog = s; plog = pr; }
-    nlog += 1;
+#ifdef SSB_PIPE_PROBE
+    if (lane == 0) C.p_arr += clock64() - pa0;
+#endif
+    if (lane == g.nlog) { g.slog = s; g.plog = pr; }
+    g.nlog += 1;
     k += 1;
-    if (nlog == 32) flush();
     if (k - k_pub >= publish_every && k < N) {
       const double tn = k < c0 + 32 ? __shfl_sync(FULL, c_t, k - c0) : __shfl_sync(FULL, n_t, k - c0 - 32);
-      publish((unsigned long long)__double_as_longlong(tn));
+#ifdef SSB_PIPE_PROBE
+      const long long pp0 = clock64();
+#endif
+      pipe_publish<BAL>(g, A, C, lane, wt_lane, (unsigned long long)__double_as_longlong(tn));
+      k_pub = k;
+#ifdef SSB_PIPE_PROBE
+      if (lane == 0) C.p_pub += clock64() - pp0;
+#endif
     }
   }
+#ifdef SSB_PIPE_PROBE
+  if (lane == 0) C.p_route = clock64() - pr0;
+#endif
   if (aborted) {
     if (lane == 0) C.abort = 1;
-    publish((unsigned long long)__double_as_longlong(INF) | SYNC_BIT);  // wake everyone
-    return;
+    pipe_publish<BAL>(g, A, C, lane, wt_lane, (unsigned long long)__double_as_longlong(INF) | SYNC_BIT);  // wake everyone
   }
-  sync(INF);  // drain: every engine to the end
 }
 
 template <int POL>
@@ -1200,7 +1296,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   const int n_al = (n + 1) & ~1;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int gw = rank * PIPE_WARPS + warp;
-  const int s = gw - 1;  // this warp's server (gw 0 routes)
+  const int s = pipe_server(gw);  // this warp's server (-1: the router or a spare warp)
   PipeCtl& C0 = rank == 0 ? C : *cl.map_shared_rank(&C, 0);
   PipeArrays A(rank == 0 ? smem_ll : cl.map_shared_rank(smem_ll, 0), n_al);
   int* const tab = (int*)((unsigned char*)smem_ll + align_up(pipe_array_bytes(n), 16)) + warp * SM_COLS * RS;
@@ -1214,6 +1310,10 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   if (threadIdx.x == 0) {
     C.wt = 0ULL;  // +0.0, no sync: nothing routed
     C.abort = C.err = C.syncs = C.polls = 0;
+#ifdef SSB_PIPE_PROBE
+    C.p_wait = C.p_route = C.p_flush = C.p_busy_sum = C.p_busy_max = C.p_wakes = C.p_iters_max = C.p_take = 0;
+    C.p_arr = C.p_pub = C.p_sync = C.p_chunk = 0;
+#endif
   }
   if (threadIdx.x < PIPE_WARPS) C.hint[threadIdx.x] = 0;
   if (rank == 0)
@@ -1239,6 +1339,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
       sn.wpend = sn.enq = sn.fc = sn.fi = sn.fo = 0;
       sn.free_b = cfg.pool;
       sn.wr = sn.next = sn._pad = 0;
+      sn.done = 0ULL;
     }
   }
   cl.sync();
@@ -1266,25 +1367,41 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
     int seen_hint = 0, taken = 0;
     double nb_lb = INF;  // lower bound of its next boundary: idle with nothing routed
     bool reported = false;
+#ifdef SSB_PIPE_PROBE
+    long long p_bs = 0, p_wk = 0, p_tk = 0;
+#endif
+#ifdef SSB_PIPE_TIMELINE
+    long long p_sy = 0;
+#endif
     volatile PipeCtl& V = C;
     const int* ring = A.ring + s * PIPE_RING;
     while (true) {
       unsigned long long w;
+      int h, nap = 32;
       while (true) {
         w = V.wt;
-        const int h = V.hint[warp];
+        acquire_smem();  // the watermark word (or the hint) is the flag of a release pattern
+        h = V.hint[warp];  // the published route count: ring slots below it are readable
         if (w != seen || h != seen_hint) {
           const double wt = __longlong_as_double((long long)(w & ~SYNC_BIT));
           if ((w & SYNC_BIT) || nb_lb < wt || h != seen_hint) break;
           seen = w;  // nothing to do before this watermark
         } else {
-          __nanosleep(32);
+          __nanosleep(nap);  // back off: polling warps share the issue slots with working ones
+          nap = nap < 256 ? 2 * nap : 256;
         }
       }
       seen = w;
-      acquire_smem();
+#ifdef SSB_PIPE_PROBE
+      const long long pe0 = clock64();
+      p_wk += 1;
+#endif
+#ifdef SSB_PIPE_TIMELINE
+      const unsigned long long tw0 = globaltimer_ns();
+      const long long it0 = E.st.iterations;
+#endif
       // take the published routes into the engine's own route list (global, rl)
-      const int cp = ld_rc_s32(&A.cnt_pub[s]);
+      const int cp = h;
       if (cp > taken) {
         int dep = 0;
         for (int b = taken; b < cp; b += 32) {
@@ -1305,10 +1422,25 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
       const bool sync = (w & SYNC_BIT) != 0;
       const double wt = __longlong_as_double((long long)(w & ~SYNC_BIT));
       if (sync && ld_rc_s32(&C0.abort)) {
-        if (lane == 0) st_rc_u64(&A.done[s], w);
+        if (lane == 0) *(volatile unsigned long long*)&C.snap[warp].done = w;
         break;
       }
+#ifdef SSB_PIPE_PROBE
+      p_tk += clock64() - pe0;
+#endif
+#ifndef SSB_PIPE_NOENGINE
+      // still in the steady state the last wake ended in (the watermark stopped it, nothing was
+      // enqueued since): continue the decode-only iterations in the tight loop right away,
+      // instead of a full step() per wake (exactly what advance_loop's first boundary would do)
+      if (E.regs_ok && E.nodisp && E.st.status == SSB_OK && E.cfg.bs_shift >= 0 && E.has_work()) {
+        const double na = E.next_arrival(taken);
+        E.fast_forward(na < wt ? na : wt);
+      }
       E.advance_loop(wt, taken);
+#endif
+#ifdef SSB_PIPE_PROBE
+      p_bs += clock64() - pe0;
+#endif
       if (E.st.status && !reported) {
         reported = true;
         if (lane == 0) st_rc_s32(&C0.err, E.st.status);
@@ -1333,12 +1465,28 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
         }
         __syncwarp();
         release_smem();
-        if (lane == 0) st_rc_u64(&A.done[s], w);
+#ifdef SSB_PIPE_TIMELINE
+        if (lane == 0 && blockIdx.x < G && p_sy < SYNC_TL_MAX && s < 128) {
+          unsigned long long* r = g_sync_tl + (long long)p_sy * SYNC_TL_W + 2 + 3 * s;
+          r[0] = tw0; r[1] = globaltimer_ns(); r[2] = (unsigned long long)(E.st.iterations - it0);
+        }
+        p_sy += 1;
+#endif
+        if (lane == 0) *(volatile unsigned long long*)&C.snap[warp].done = w;
         if (!(wt < INF)) break;
       }
     }
     E.drop_regs();
     if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
+#ifdef SSB_PIPE_PROBE
+    if (lane == 0) {
+      atomicAdd(&C0.p_busy_sum, (unsigned long long)p_bs);
+      atomicMax(&C0.p_busy_max, (unsigned long long)p_bs);
+      atomicAdd(&C0.p_wakes, (unsigned long long)p_wk);
+      atomicAdd(&C0.p_take, (unsigned long long)p_tk);
+      atomicMax(&C0.p_iters_max, (unsigned long long)E.st.iterations);
+    }
+#endif
   }
   cl.sync();  // every engine's state is in memory; rank 0's shared memory outlives its readers
 
@@ -1370,6 +1518,9 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
 #ifdef SSB_PIPE_PROBE
     out._pad = C.syncs;            // diagnostics: engine syncs (routing epochs)
     out.device_cycles = C.polls;   //              view refreshes
+    printf("PIPE inst %d n %d N %lld syncs %d polls %d | router total %llu wait %llu flush %llu | engines busy sum %llu max %llu "
+           "wakes %llu take %llu iters_max %llu | per-arrival %llu publish %llu sync %llu chunk %llu\n", idx, n, N, C.syncs, C.polls, C.p_route, C.p_wait, C.p_flush,
+           C.p_busy_sum, C.p_busy_max, C.p_wakes, C.p_take, C.p_iters_max, C.p_arr, C.p_pub, C.p_sync, C.p_chunk);
 #endif
     stats[idx] = out;
     if (ev_count) ev_count[idx] = evn;
@@ -1649,9 +1800,9 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   if (!multis_done && max_servers <= PIPE_MAX_SERVERS && getenv("SSB_CLUSTER_CLASSIC") == nullptr) {
     // pipelined: one cluster of G CTAs x 8 warps per instance, a routing warp + one warp per
     // replica (G = 9 for 64 replicas: a non-portable cluster size)
-    const int G = (max_servers + 1 + PIPE_WARPS - 1) / PIPE_WARPS;
-    int publish_every = 8;
-    if (const char* e = getenv("SSB_PIPE_PUBLISH")) publish_every = std::max(1, atoi(e));  // experiments
+    const int G = 1 + (max_servers + PIPE_WARPS - 1) / PIPE_WARPS;
+    int publish_every = 8;  // <= 32: the route log is one lane per route
+    if (const char* e = getenv("SSB_PIPE_PUBLISH")) publish_every = std::min(32, std::max(1, atoi(e)));  // experiments
     const size_t smc = align_up(pipe_array_bytes(max_servers), 16) + sizeof(int) * SM_COLS * RS * PIPE_WARPS;
     cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
     if (G > 8) cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1719,6 +1870,13 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   return SSB_OK;
 }
 
+#ifdef SSB_PIPE_TIMELINE
+extern "C" int32_t ssb_debug_sync_timeline(unsigned long long* out, int32_t n_syncs) {
+  if (n_syncs > SYNC_TL_MAX) n_syncs = SYNC_TL_MAX;
+  return cudaMemcpyFromSymbol(out, g_sync_tl, sizeof(unsigned long long) * SYNC_TL_W * (size_t)n_syncs) == cudaSuccess
+             ? n_syncs : -1;
+}
+#endif
 #ifdef SSB_TIMELINE
 extern "C" int32_t ssb_debug_timeline(unsigned long long* out, int32_t n) {
   if (n > TIMELINE_MAX) n = TIMELINE_MAX;
