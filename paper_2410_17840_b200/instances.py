@@ -151,52 +151,58 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
     resolved engine limits), and the instance descriptor once per settings
     object (then copied with this job's offsets and factor)."""
     traces: list[Trace] = []
-    trace_index: dict[int, int] = {}
+    trace_index: dict[int, int] = {}  # id(trace) -> [index, offset, length]
     keep_alive: list = []  # every keyed object lives until the loop ends, so no id() is reused
-    trace_offs: list[int] = []
-    base: dict[int, list] = {}  # id(settings) -> [ResolvedEngine, template index]
+    base: dict[int, list] = {}  # id(settings) -> [ResolvedEngine, template index, feasibility key]
     templates: list = []
     feasible: set = set()
-    rows: list = []
+    c_tpl: list = []
+    c_n: list = []
+    c_toff: list = []
+    c_roff: list = []
+    c_fac: list = []
     labels = []
     n_trace = 0
     n_records = 0
+    isfinite = math.isfinite
     for job in jobs:
-        settings, trace, factor = job[0], job[1], float(job[2]) if len(job) > 2 else 1.0
-        label = job[3] if len(job) > 3 else None
-        key = id(trace)
-        if key not in trace_index:
+        trace = job[1]
+        nj = len(job)
+        factor = float(job[2]) if nj > 2 else 1.0
+        if not (factor > 0 and isfinite(factor)):
+            check_qps_factor(factor)  # raises the reference's error
+        tr = trace_index.get(id(trace))
+        if tr is None:
             t = as_trace(trace)
             t.validate()
             keep_alive.append(trace)
-            trace_index[key] = len(traces)
+            tr = trace_index[id(trace)] = [len(traces), n_trace, len(t)]
             traces.append(t)
-            trace_offs.append(n_trace)
-            n_trace += len(t)
-        ti = trace_index[key]
-        t = traces[ti]
-        toff = trace_offs[ti]
-        sk = id(settings)
-        if sk not in base:  # build_engine first (cluster.py:74-79), the balancer after the checks (:96-104)
+            n_trace += tr[2]
+        settings = job[0]
+        bs = base.get(id(settings))
+        if bs is None:  # build_engine first (cluster.py:74-79), the balancer after the checks (:96-104)
             keep_alive.append(settings)
             r = resolve_engine(settings.engine)
             lim = r.limits
-            base[sk] = [r, None, (policy_descriptor(r.policy), r.block_size, r.pool_blocks,
-                                  lim.max_tokens_per_batch, lim.max_running, lim.max_context)]
-        re = base[sk][0]
-        factor = check_qps_factor(factor)
+            bs = base[id(settings)] = [r, -1, (policy_descriptor(r.policy), r.block_size, r.pool_blocks,
+                                               lim.max_tokens_per_batch, lim.max_running, lim.max_context)]
         if validate:
-            lim = re.limits
-            fk = (ti, base[sk][2])
+            fk = (tr[0], bs[2])
             if fk not in feasible:
-                re.policy.check_feasible_many(t.prompt, t.output, re.block_size, re.pool_blocks, lim)
+                re, t = bs[0], traces[tr[0]]
+                re.policy.check_feasible_many(t.prompt, t.output, re.block_size, re.pool_blocks, re.limits)
                 feasible.add(fk)
-        if base[sk][1] is None:
-            base[sk][1] = len(templates)
-            templates.append(instance_record(settings, 0, resolved=re))
-        rows.append((base[sk][1], len(t), toff, n_records, factor))
-        labels.append(label)
-        n_records += len(t)
+        if bs[1] < 0:  # the balancer's checks come after feasibility (cluster.py:90-104)
+            bs[1] = len(templates)
+            templates.append(instance_record(settings, 0, resolved=bs[0]))
+        c_tpl.append(bs[1])
+        c_n.append(tr[2])
+        c_toff.append(tr[1])
+        c_roff.append(n_records)
+        c_fac.append(factor)
+        labels.append(job[3] if nj > 3 else None)
+        n_records += tr[2]
     if traces:
         trace_all = Trace(
             np.concatenate([t.arrival for t in traces]),
@@ -205,13 +211,12 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
         )
     else:
         trace_all = Trace(np.zeros(0), np.zeros(0), np.zeros(0))
-    if rows:
-        ti, n, toff, roff, fac = (np.array(c) for c in zip(*rows))
-        inst = np.array(templates, dtype=_abi.INSTANCE)[ti]
-        inst["n_requests"] = n
-        inst["trace_offset"] = toff
-        inst["record_offset"] = roff
-        inst["qps_factor"] = fac.astype(np.float64)
+    if c_tpl:
+        inst = np.array(templates, dtype=_abi.INSTANCE)[np.array(c_tpl)]
+        inst["n_requests"] = c_n
+        inst["trace_offset"] = c_toff
+        inst["record_offset"] = c_roff
+        inst["qps_factor"] = np.array(c_fac, dtype=np.float64)
     else:
         inst = np.zeros(0, dtype=_abi.INSTANCE)
     return Batch(trace_all, inst, n_records, labels)
