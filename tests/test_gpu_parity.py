@@ -105,3 +105,56 @@ def test_gpu_event_ring_overflow_reruns():
         for s, want_s in enumerate(golden[sc["name"]]["events"]):
             got = [(int(e["code"]), int(e["request_id"]), float(e["time"])) for e in ev[s]]
             assert got == [tuple(e) for e in want_s], (sc["name"], s)
+
+
+@pytest.mark.parametrize("group", ["cluster_unit", "fuzz_cluster", "fuzz_multicta"])
+def test_gpu_classic_epoch_kernel_matches_reference(group, monkeypatch):
+    """The r01 epoch kernel (k_cluster: routing phase / cluster barrier / advance phase) still
+    serves clusters above the pipelined kernel's 120 replicas; SSB_CLUSTER_CLASSIC=1 routes
+    every cluster to it so it keeps its reference parity coverage."""
+    monkeypatch.setenv("SSB_CLUSTER_CLASSIC", "1")
+    golden = load_golden(group)
+    scs = S.GROUPS[group]()
+    batch = scenario_batch(scs)
+    rec, stats, est = _sim().run_batch(batch, with_engines=True)
+    rows = np.concatenate([[0], np.cumsum(batch.instances["n_servers"])])
+    bad = {}
+    for i, sc in enumerate(scs):
+        f = compare_instance(sc, golden, batch, i, rec, stats, engines=est[rows[i]:rows[i + 1]])
+        if f:
+            bad[sc["name"]] = f
+    assert not bad, f"{len(bad)} mismatches: " + repr(dict(list(bad.items())[:4]))
+
+
+@pytest.mark.parametrize("publish", ["1", "32"])
+def test_gpu_pipelined_kernel_publish_period_is_result_free(publish, monkeypatch):
+    """The watermark publish period only changes how far the engines trail the router,
+    never a decision: the extreme periods give the reference's results."""
+    monkeypatch.setenv("SSB_PIPE_PUBLISH", publish)
+    golden = load_golden("fuzz_multicta")
+    scs = S.GROUPS["fuzz_multicta"]()
+    batch = scenario_batch(scs)
+    rec, stats, est = _sim().run_batch(batch, with_engines=True)
+    rows = np.concatenate([[0], np.cumsum(batch.instances["n_servers"])])
+    for i, sc in enumerate(scs):
+        assert not compare_instance(sc, golden, batch, i, rec, stats, engines=est[rows[i]:rows[i + 1]]), sc["name"]
+
+
+def test_gpu_cluster_above_pipeline_limit_matches_oracle():
+    """130 replicas (more than the pipelined kernel's 120: the epoch kernel with several
+    replicas per warp and global tables) under sal and p2c, against the oracle."""
+    from oracle import oracle as O
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200.settings import BalancerSettings, ClusterSettings, EngineSettings
+    from paper_2410_17840_b200.workload import SynthSpec, synthesize
+
+    trace = synthesize(SynthSpec(duration_s=30.0, mean_qps=90.0, burstiness=2.0, seed=11))
+    jobs = [(ClusterSettings(130, EngineSettings(policy=pol, pool_blocks=700), BalancerSettings(bal, poll_interval_s=0.02), 5),
+             trace, 1.0) for pol, bal in (("larry", "sal"), ("trail_plus", "p2c"), ("fcfs", "rr"))]
+    batch = I.make_batch(jobs)
+    rec, st = _sim().run_batch(batch, check=True)
+    orec, ost = O.run_batch(batch, threads=3)
+    for k in ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "finished", "digest", "status"):
+        assert np.array_equal(st[k], ost[k]), k
+    for col in ("first_token", "finish", "preempt_count", "server"):
+        assert np.array_equal(getattr(rec, col), getattr(orec, col)), col
