@@ -121,8 +121,6 @@ struct SrvPtr {
   int* rl;    // route list (arrival ids routed to this engine), n_servers > 1
   int* t_head;  // trail_plus: first request id of each remaining-output bucket (-1 = empty)
   int* t_lv;    // trail_plus: min-need tree over the buckets (level 0 = per-bucket minimum)
-  int* t_top;   // its top level (one chunk of <= 128 nodes): shared memory beside the running table
-                // when the engine has one (else global, = t_lv + level offset of the top)
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -404,19 +402,16 @@ struct Eng {
   __device__ void trail_init() {
     for (int i = lane; i < cfg.tg.nb; i += 32) p.t_head[i] = -1;
     for (int i = lane; i < cfg.tg.total; i += 32) p.t_lv[i] = 0x7fffffff;
-    for (int i = lane; i < TF; i += 32) p.t_top[i] = 0x7fffffff;
     __syncwarp();
   }
   // level offset without dynamic indexing (keeps Cfg in registers)
   __device__ __forceinline__ int t_off(int l) const {
     return l == 0 ? 0 : (l == 1 ? cfg.tg.off[1] : cfg.tg.off[2]);
   }
-  // a level's node array: the top level in t_top (shared memory), the others in global t_lv
-  __device__ __forceinline__ int* t_level(int l) const { return l == cfg.tg.top ? p.t_top : p.t_lv + t_off(l); }
-  // first node of the 128-node chunk at `chunk` (int offset into `lv`) with value <= T and index
-  // >= lo (chunk-relative), or -1: lane i holds nodes 4i..4i+3
-  __device__ __forceinline__ int t_chunk_first(const int* lv, int chunk, int lo, int T) const {
-    const int4 v = *reinterpret_cast<const int4*>(lv + chunk + 4 * lane);
+  // first node of the 128-node chunk at `chunk` (int offset) with value <= T and index >= lo
+  // (chunk-relative), or -1: lane i holds nodes 4i..4i+3
+  __device__ __forceinline__ int t_chunk_first(int chunk, int lo, int T) const {
+    const int4 v = *reinterpret_cast<const int4*>(p.t_lv + chunk + 4 * lane);
     const int q = 4 * lane;
     const unsigned bits = (unsigned)(v.x <= T && q >= lo) | ((unsigned)(v.y <= T && q + 1 >= lo) << 1) |
                           ((unsigned)(v.z <= T && q + 2 >= lo) << 2) | ((unsigned)(v.w <= T && q + 3 >= lo) << 3);
@@ -429,21 +424,13 @@ struct Eng {
   // first bucket >= b0 whose minimum need is <= T, or -1. Climb from b0's chunk until a
   // node <= T follows it, then descend (some child of a node <= T is <= T). One loop with a
   // single chunk probe: the probe is inlined once (the engine is instruction-fetch bound).
-  // With two levels the top is in shared memory: b0's parent there says whether b0's chunk
-  // can hold a candidate at all, so a search usually costs one global probe instead of three.
   __device__ int t_find(int b0, int T) const {
     if (b0 >= cfg.tg.nb) return -1;
     int lvl = 0, idx = b0, base = b0 & ~(TF - 1), lo = b0 & (TF - 1);
     bool down = false;
-    if (cfg.tg.top == 1 && p.t_top[b0 >> TF_SHIFT] > T) {  // nothing in b0's chunk: start at the top
-      lvl = 1;
-      idx = b0 >> TF_SHIFT;
-      base = 0;
-      lo = idx + 1;
-    }
     #pragma unroll 1
     while (true) {
-      const int r = t_chunk_first(t_level(lvl), base, lo, T);
+      const int r = t_chunk_first(t_off(lvl) + base, lo, T);
       if (down || r >= 0) {  // (descending, r >= 0 always holds)
         const int node = base + r;
         if (lvl == 0) return node;
@@ -463,20 +450,19 @@ struct Eng {
 
   // set bucket b's minimum and restore "node = min of children" up the tree
   __device__ void t_set_leaf(int b, int val) {
-    int* const l0 = t_level(0);
-    if (l0[b] == val) return;
+    if (p.t_lv[b] == val) return;
     __syncwarp();
-    if (lane == 0) l0[b] = val;
+    if (lane == 0) p.t_lv[b] = val;
     __syncwarp();
     int idx = b;
     for (int l = 1; l <= cfg.tg.top; ++l) {
       const int parent = idx >> TF_SHIFT;
-      const int4 v = *reinterpret_cast<const int4*>(t_level(l - 1) + (parent << TF_SHIFT) + 4 * lane);
+      const int4 v = *reinterpret_cast<const int4*>(p.t_lv + t_off(l - 1) + (parent << TF_SHIFT) + 4 * lane);
       const int mn = __reduce_min_sync(FULL, min(min(v.x, v.y), min(v.z, v.w)));
-      int* const lv = t_level(l);
-      if (lv[parent] == mn) break;
+      const int at = t_off(l) + parent;
+      if (p.t_lv[at] == mn) break;
       __syncwarp();
-      if (lane == 0) lv[parent] = mn;
+      if (lane == 0) p.t_lv[at] = mn;
       __syncwarp();
       idx = parent;
     }
@@ -493,7 +479,7 @@ struct Eng {
     }
     __syncwarp();
     const int need = blocks(pend);
-    if (need < t_level(0)[rem]) t_set_leaf(rem, need);
+    if (need < p.t_lv[rem]) t_set_leaf(rem, need);
     st.W += 1;
   }
   // unlink `cur` (predecessor `prev`, -1 = head) from bucket b; `need` = its block need
@@ -502,7 +488,7 @@ struct Eng {
     __syncwarp();
     if (lane == 0) { if (prev < 0) p.t_head[b] = nx; else p.w_rid[prev] = nx; }
     __syncwarp();
-    if (need == t_level(0)[b]) {  // it may have been the minimum: recompute the bucket's
+    if (need == p.t_lv[b]) {  // it may have been the minimum: recompute the bucket's
       int mn = 0x7fffffff;
       for (int c = p.t_head[b]; c >= 0; c = t_next(c)) mn = min(mn, blocks(t_pend(c) & 0x7fffffff));
       t_set_leaf(b, mn);
@@ -883,7 +869,7 @@ struct Eng {
         if (V > 0) {  // exact threshold of the found bucket
           T = (long long)free + victims_gain(V, vk, vb, b);
           if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
-          if (t_level(0)[b] > T) { b += 1; continue; }
+          if (p.t_lv[b] > T) { b += 1; continue; }
         }
       }
       SSB_T0(wk)

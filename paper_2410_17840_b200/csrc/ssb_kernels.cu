@@ -147,8 +147,6 @@ __device__ inline void init_srv(Srv& s, const Cfg& c) {
 // v_idx v_rem v_cum(2) v_key(2) l_c
 constexpr int SM_COLS = 16;
 constexpr int RS = SSB_SMEM_RUN_CAP;
-// per-engine shared-memory block: the running table, then the top level of the trail_plus tree
-constexpr int TAB_INTS = SM_COLS * RS + TF;
 
 // sm_tab: this engine's shared-memory running table (SM_COLS x RS ints) or
 // nullptr for the global layout (SSB_FLAG_GLOBAL_TABLES).
@@ -157,9 +155,6 @@ __device__ inline void bind_engine(Eng& E, const ssb_instance& I, const Cfg& cfg
                                    int* sm_tab = nullptr) {
   E.cfg = cfg;
   E.p = make_ptrs(scratch + I.scratch_offset + (long long)server * L.total, L);
-  // the tree's top level: beside the running table in shared memory when there is one
-  E.p.t_top = sm_tab != nullptr ? sm_tab + SM_COLS * RS
-                                : E.p.t_lv + (cfg.tg.top == 0 ? 0 : (cfg.tg.top == 1 ? cfg.tg.off[1] : cfg.tg.off[2]));
   if (sm_tab != nullptr && !(I.flags & SSB_FLAG_GLOBAL_TABLES)) {
     E.p.r_rid = sm_tab;
     E.p.r_prompt = sm_tab + RS;
@@ -348,7 +343,7 @@ k_engines(const ssb_instance* __restrict__ inst, const int* __restrict__ order, 
           int64_t* ev_count) {
   extern __shared__ int sm_engines[];
   __shared__ int s_slot;
-  int* sm_tab = sm_engines + (threadIdx.x >> 5) * TAB_INTS;  // this warp's running table
+  int* sm_tab = sm_engines + (threadIdx.x >> 5) * (SM_COLS * RS);  // this warp's running table
   const int lane = lane_id();
   const unsigned smid = sm_id();
   const int first = known_sm(smid, n_sm_policy) ? sm_policy[smid] : 0;
@@ -518,7 +513,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
   // cluster barrier (also orders the DSMEM and global accesses around it); a one-CTA
   // cluster (<= 8 replicas) uses the cheaper CTA barrier
   auto csync = [&]() { if (G == 1) __syncthreads(); else cl.sync(); };
-  auto tab_of = [&](int s) { return tabs_in_smem ? sm_tabs + ((s / GW) * nwarps + warp) * TAB_INTS : nullptr; };
+  auto tab_of = [&](int s) { return tabs_in_smem ? sm_tabs + ((s / GW) * nwarps + warp) * SM_COLS * RS : nullptr; };
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;
   const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
@@ -1326,7 +1321,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   const int s = pipe_server(gw);  // this warp's server (-1: the router or a spare warp)
   PipeCtl& C0 = rank == 0 ? C : *cl.map_shared_rank(&C, 0);
   PipeArrays A(rank == 0 ? smem_ll : cl.map_shared_rank(smem_ll, 0), n_al);
-  int* const tab = (int*)((unsigned char*)smem_ll + align_up(pipe_array_bytes(n), 16)) + warp * TAB_INTS;
+  int* const tab = (int*)((unsigned char*)smem_ll + align_up(pipe_array_bytes(n), 16)) + warp * SM_COLS * RS;
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;
   const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
@@ -1839,7 +1834,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const int G = 1 + (max_servers + PIPE_WARPS - 1) / PIPE_WARPS;
     int publish_every = 8;  // <= 32: the route log is one lane per route
     if (const char* e = getenv("SSB_PIPE_PUBLISH")) publish_every = std::min(32, std::max(1, atoi(e)));  // experiments
-    const size_t smc = align_up(pipe_array_bytes(max_servers), 16) + sizeof(int) * TAB_INTS * PIPE_WARPS;
+    const size_t smc = align_up(pipe_array_bytes(max_servers), 16) + sizeof(int) * SM_COLS * RS * PIPE_WARPS;
     cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
     if (G > 8) cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t lc = {};
@@ -1868,7 +1863,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const int per_warp = (max_servers + G * nw - 1) / (G * nw);  // replicas per warp
     const int tabs = per_warp * nw <= CLUSTER_SMEM_SERVERS ? 1 : 0;
     size_t smc = sizeof(long long) * 6 * ((max_servers + 1) & ~1);
-    if (tabs) smc += sizeof(int) * TAB_INTS * per_warp * nw;
+    if (tabs) smc += sizeof(int) * SM_COLS * RS * per_warp * nw;
     if (smc > 48 * 1024) cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(multis.size() * G));
@@ -1892,7 +1887,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const bool wide = (int)singles.size() <= sms && getenv("SSB_NO_LATENCY_MODE") == nullptr;
     auto kern = wide ? k_engines<true> : k_engines<false>;
     int occ = 1;
-    const size_t sm = sizeof(int) * TAB_INTS * ENGINE_WARPS_PER_CTA;
+    const size_t sm = sizeof(int) * SM_COLS * RS * ENGINE_WARPS_PER_CTA;
     if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * ENGINE_WARPS_PER_CTA, sm);
     if (const char* cap = getenv("SSB_CTAS_PER_SM")) occ = std::min(occ, std::max(1, atoi(cap)));  // experiments
