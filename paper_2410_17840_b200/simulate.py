@@ -64,13 +64,12 @@ def cost_features(batch: Batch) -> np.ndarray:
     ctx = pm + qm / 2
     # nopreempt: mean reservation, min(max_context, prompt + max_output) per request
     res = ctx.copy()
-    seen: dict = {}  # sweeps repeat (trace slice, limits) across many instances
-    for i in np.flatnonzero(e["policy"] == 1):
-        key = (o[i], n[i], mc[i], mo[i])
-        if key not in seen:
-            seg = p[o[i]:o[i] + n[i]]
-            seen[key] = np.minimum(mc[i], seg + mo[i]).mean() if n[i] else ctx[i]
-        res[i] = seen[key]
+    npm = e["policy"] == 1
+    if npm.any():  # per distinct (max_context, max_output): one clipped prefix sum over the whole trace
+        for mci, moi in {(float(a), float(b)) for a, b in zip(mc[npm], mo[npm])}:
+            sel = npm & (mc == mci) & (mo == moi)
+            cr = np.concatenate([[0.0], np.cumsum(np.minimum(mci, p + moi))])
+            res[sel] = np.where(n[sel] > 0, (cr[o[sel] + n[sel]] - cr[o[sel]]) / nz[sel], ctx[sel])
     last = np.where(n > 0, tr.arrival[np.minimum(o + np.maximum(n - 1, 0), max(len(tr.arrival) - 1, 0))], 0.0)
     first = np.where(n > 0, tr.arrival[np.minimum(o, max(len(tr.arrival) - 1, 0))], 0.0)
     span = np.maximum((last - first) / inst["qps_factor"], 1e-9)
