@@ -125,3 +125,33 @@ def test_c3_full_size_matches_oracle_golden():
         for col, sha in want["records_sha256"].items():
             got = hashlib.sha256(np.ascontiguousarray(getattr(rec, col)[o:o + n]).tobytes()).hexdigest()
             assert got == sha, (want["label"], col)
+
+
+def test_running_table_overflow_reruns_with_global_tables():
+    """More than 256 running requests on one engine (the shared-memory running table's
+    capacity): the kernel reports SSB_E_CAPACITY, the host re-runs that instance with global
+    tables (k_engines and the pipelined cluster kernel), and the results equal the oracle's."""
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200 import simulate
+    from paper_2410_17840_b200.settings import BalancerSettings, ClusterSettings, EngineSettings
+    from paper_2410_17840_b200.workload import Trace
+
+    n = 1500
+    rng = np.random.default_rng(3)
+    arr = np.sort(np.round(rng.uniform(0.0, 0.5, n), 2))
+    trace = Trace(arr, rng.integers(1, 8, n), rng.integers(5, 60, n))
+    jobs = [(ClusterSettings(1, EngineSettings(policy="fcfs", pool_blocks=60_000), BalancerSettings("rr"), 0), trace, 1.0),
+            (ClusterSettings(2, EngineSettings(policy="larry", pool_blocks=60_000), BalancerSettings("sal", poll_interval_s=0.05), 1),
+             trace, 1.0),
+            (ClusterSettings(2, EngineSettings(policy="trail_plus", c=0.5, pool_blocks=60_000), BalancerSettings("rr"), 2),
+             trace, 1.0)]
+    batch = I.make_batch(jobs)
+    db, _ = simulate.simulate_batch(batch)
+    assert (db.h_inst["flags"] & 1).all(), "every instance should have overflowed its shared table"
+    rec, st = simulate.download(db)
+    assert int(st["peak_batch_tokens"].max()) > 256
+    orec, ost = O.run_batch(batch, threads=3)
+    for k in KEYS:
+        assert np.array_equal(st[k], ost[k]), k
+    for col in ("first_token", "finish", "preempt_count", "server"):
+        assert np.array_equal(getattr(rec, col), getattr(orec, col)), col
