@@ -1849,6 +1849,12 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    if (getenv("SSB_DEBUG_CLUSTERS")) {  // diagnostics: how many of these clusters fit the GPU at once
+      int nc = -1;
+      cudaOccupancyMaxActiveClusters(&nc, k_cluster_pipe, &lc);
+      fprintf(stderr, "k_cluster_pipe: %zu clusters of %d CTAs x %d threads, %zu B shared each; max active clusters %d\n",
+              multis.size(), G, 32 * PIPE_WARPS, smc, nc);
+    }
     if (cudaLaunchKernelEx(&lc, k_cluster_pipe, (const ssb_instance*)d_inst, (const int*)(d_hdr + off_multi), trace,
                            records, d_stats, scratch, d_events, (long long)event_cap, (int64_t*)d_event_count,
                            publish_every) == cudaSuccess)
