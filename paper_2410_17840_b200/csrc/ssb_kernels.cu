@@ -967,20 +967,18 @@ struct PipeCtl {
 
 // rank 0's dynamic shared memory, per server (n_al = n rounded up to even)
 struct PipeArrays {
-  unsigned long long* done;  // engine -> router: the last sync word it reached
-  long long* rps;            // Σ prompt routed (router)
-  int *cnt, *cnt_pub, *taken;  // routed / published / taken by the engine
-  int* ring;                 // [n][PIPE_RING] routed arrival ids
+  long long* rps;    // Σ prompt routed (router)
+  int *cnt, *taken;  // routed (router) / taken by the engine (engine -> router, flow control)
+  int* ring;         // [n][PIPE_RING] routed arrival ids
   __device__ PipeArrays(long long* b, int n_al) {
-    done = (unsigned long long*)b;
-    rps = b + n_al;
-    int* ib = (int*)(b + 2 * n_al);
-    cnt = ib; cnt_pub = ib + n_al; taken = ib + 2 * n_al;
-    ring = ib + 4 * n_al;
+    rps = b;
+    int* ib = (int*)(b + n_al);
+    cnt = ib; taken = ib + n_al;
+    ring = ib + 2 * n_al;
   }
 };
 __host__ __device__ constexpr long long pipe_array_bytes(int n) {
-  return 8LL * 2 * ((n + 1) & ~1) + 4LL * 4 * ((n + 1) & ~1) + 4LL * PIPE_RING * n;
+  return 8LL * ((n + 1) & ~1) + 4LL * 2 * ((n + 1) & ~1) + 4LL * PIPE_RING * n;
 }
 
 // the routing warp. Plain locals and force-inlined helpers that take them by reference
@@ -1340,9 +1338,8 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   if (threadIdx.x < PIPE_WARPS) C.hint[threadIdx.x] = 0;
   if (rank == 0)
     for (int q = threadIdx.x; q < n; q += blockDim.x) {
-      A.done[q] = 0ULL;
       A.rps[q] = 0;
-      A.cnt[q] = A.cnt_pub[q] = A.taken[q] = 0;
+      A.cnt[q] = A.taken[q] = 0;
     }
   {
     Eng E;
