@@ -191,3 +191,25 @@ def test_vectorised_summary_ranks_equal_python_nearest_rank():
         want = np.array([math.ceil(p / 100 * int(n)) for n in ns])
         assert np.array_equal(g["rank"][:, j], want), p
     assert (g["rank"][:, 3:] == 0).all()
+
+
+def test_first_run_cost_model_is_a_sane_hint():
+    """simulate.estimate_cost (the first-run placement hint, fit on measured iterations): one
+    coefficient row per policy over cost_design's columns, positive finite int64 estimates, the
+    expensive policy first on average (trail_plus: ~3.5k device cycles per iteration vs
+    nopreempt's ~330), deterministic, and a work proxy for clusters."""
+    import numpy as np
+
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200 import instances as I
+    from paper_2410_17840_b200 import simulate
+
+    jobs = C.c4_jobs(seeds=[3])
+    b = I.make_batch(jobs)
+    assert simulate.ITER_COEF.shape == (4, simulate.cost_design(b).shape[1])
+    c = simulate.estimate_cost(b)
+    assert c.dtype == np.int64 and (c >= 1).all() and (c < 2**31).all()
+    assert np.array_equal(c, simulate.estimate_cost(I.make_batch(jobs)))
+    pol = np.array([j[3].split("/")[1] for j in jobs])
+    assert c[pol == "trail_plus"].mean() > 3 * c[pol == "nopreempt"].mean()
+    assert (simulate.estimate_cost(I.make_batch(C.c2_jobs(60.0))) >= 1).all()
