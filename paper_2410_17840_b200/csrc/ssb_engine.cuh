@@ -428,6 +428,27 @@ struct Eng {
     if (b0 >= cfg.tg.nb) return -1;
     int lvl = 0, idx = b0, base = b0 & ~(TF - 1), lo = b0 & (TF - 1);
     bool down = false;
+    if (cfg.tg.top == 1) {
+      // two levels (up to 16,384 buckets): b0's chunk and the top chunk probed at once (both
+      // loads in flight together), so a search that has to climb costs two rounds, not three
+      const int4 v = *reinterpret_cast<const int4*>(p.t_lv + base + 4 * lane);
+      const int4 u = *reinterpret_cast<const int4*>(p.t_lv + cfg.tg.off[1] + 4 * lane);
+      const int q = 4 * lane, lo1 = (b0 >> TF_SHIFT) + 1;
+      const unsigned b0s = (unsigned)(v.x <= T && q >= lo) | ((unsigned)(v.y <= T && q + 1 >= lo) << 1) |
+                           ((unsigned)(v.z <= T && q + 2 >= lo) << 2) | ((unsigned)(v.w <= T && q + 3 >= lo) << 3);
+      const unsigned b1s = (unsigned)(u.x <= T && q >= lo1) | ((unsigned)(u.y <= T && q + 1 >= lo1) << 1) |
+                           ((unsigned)(u.z <= T && q + 2 >= lo1) << 2) | ((unsigned)(u.w <= T && q + 3 >= lo1) << 3);
+      const unsigned m0 = __ballot_sync(FULL, b0s != 0u);
+      if (m0 != 0u) {
+        const int f = __ffs(m0) - 1;
+        return base + 4 * f + __ffs(__shfl_sync(FULL, b0s, f)) - 1;
+      }
+      const unsigned m1 = __ballot_sync(FULL, b1s != 0u);
+      if (m1 == 0u) return -1;
+      const int f = __ffs(m1) - 1;
+      const int node = 4 * f + __ffs(__shfl_sync(FULL, b1s, f)) - 1;
+      return (node << TF_SHIFT) + t_chunk_first(node << TF_SHIFT, 0, T);  // a child of a node <= T is <= T
+    }
     #pragma unroll 1
     while (true) {
       const int r = t_chunk_first(t_off(lvl) + base, lo, T);
