@@ -472,6 +472,7 @@ def c5_figure(steps: int) -> dict:
     keys = ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "finished", "digest", "status")
     t = statistics.median(ts)
     return {"value": rs / t, "unit": UNIT, "seconds_per_launch": t, "clusters": len(jobs), "replicas": 64,
+            "kernel": "k_cluster_pipe: one 9-CTA thread-block cluster per instance (routing warp + 64 engine warps)",
             "requests": int(batch.n_records), "request_steps": rs, "prefix_s": C5_PREFIX_S,
             "oracle": {"value": rs / dt, "seconds": dt, "threads": threads, "kind": "port"},
             "gpu_over_oracle": dt / t,
