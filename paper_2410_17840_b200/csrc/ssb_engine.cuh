@@ -503,9 +503,8 @@ struct Eng {
     if (need < p.t_lv[rem]) t_set_leaf(rem, need);
     st.W += 1;
   }
-  // unlink `cur` (predecessor `prev`, -1 = head) from bucket b; `need` = its block need
-  __device__ void trail_remove(int b, int prev, int cur, int need) {
-    const int nx = t_next(cur);
+  // unlink `cur` (predecessor `prev`, -1 = head; successor `nx`) from bucket b; `need` = its block need
+  __device__ void trail_remove(int b, int prev, int cur, int nx, int need) {
     __syncwarp();
     if (lane == 0) { if (prev < 0) p.t_head[b] = nx; else p.w_rid[prev] = nx; }
     __syncwarp();
@@ -873,6 +872,7 @@ struct Eng {
     SSB_T1(vb, 8)
     int free = st.free_blocks;
     int b = 0, after = -1;  // resume point: bucket b, ids > after
+    int r_prev = -1, r_cur = -1;  // ... and where its list continues after the last dispatch from b
     while (true) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;  // :179-181
       long long T = (long long)free + (V > 0 ? victims_gain(V, vk, vb, b) : 0);
@@ -894,17 +894,21 @@ struct Eng {
         }
       }
       SSB_T0(wk)
-      int prev = -1, cur = p.t_head[b], pv = 0, need = 0;
-      while (cur >= 0 && cur <= after) { prev = cur; cur = t_next(cur); }
+      // the walk resumes behind the last dispatch from this bucket (its entries before that
+      // were not admissible then, with a larger free pool, so they are not now) instead of
+      // re-walking the list from its head; next and pending of an entry are loaded together
+      int prev = -1, cur = after >= 0 ? r_cur : p.t_head[b], pv = 0, need = 0, nx = -1;
+      if (after >= 0) prev = r_prev;
       while (cur >= 0) {
 #ifdef SSB_PHASE_TIMING
         tm[6] += 1;
 #endif
         pv = t_pend(cur);
+        nx = t_next(cur);
         need = blocks(pv & 0x7fffffff);
         if ((long long)need <= T) break;
         prev = cur;
-        cur = t_next(cur);
+        cur = nx;
       }
       SSB_T1(wk, 10)
       if (cur < 0) { b += 1; after = -1; continue; }
@@ -930,9 +934,11 @@ struct Eng {
       free -= need;
       __syncwarp();
       SSB_T0(rm)
-      trail_remove(b, prev, cur, need);
+      trail_remove(b, prev, cur, nx, need);
       SSB_T1(rm, 11)
       after = cur;
+      r_prev = prev;
+      r_cur = nx;
     }
     __syncwarp();
     nd_out = nd;
