@@ -200,7 +200,9 @@ size_t ssb_prepare(ssb_instance* h_inst, int32_t n_inst);
 
 /* Simulate n_inst instances. h_inst: the prepared host descriptors (launch
  * planning: instances with n_servers == 1 run one per warp in a persistent
- * kernel, longest est_cost first; multi-server instances run one per CTA).
+ * kernel, longest est_cost first; a multi-server instance runs on one
+ * thread-block cluster: a routing warp + one engine warp per replica up to 120
+ * replicas (k_cluster_pipe), the epoch kernel k_cluster beyond).
  * d_inst: device copy of the same array. d_scratch: ssb_prepare() bytes.
  * d_events (nullable): per-instance event ring of event_cap entries each,
  * instance i writes [i*event_cap, (i+1)*event_cap); d_event_count (nullable
