@@ -1277,6 +1277,31 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
 #ifdef SSB_PIPE_PROBE
     if (lane == 0) C.p_arr += clock64() - pa0;
 #endif
+    if (publish_every == 1 && k + 1 < N) {
+      // streamlined publish of one route (no log, no match_any): the ring slot, one release,
+      // the wake hint and the watermark = the next arrival's time
+      cg::cluster_group cl = cg::this_cluster();
+      const int base = A.cnt[s];
+      while (base + 1 - *(volatile int*)&A.taken[s] > PIPE_RING) __nanosleep(64);  // flow control
+      if (lane == 0) {
+        A.ring[s * PIPE_RING + (base & (PIPE_RING - 1))] = k;
+        if (BAL == SSB_BAL_SAL || BAL == SSB_BAL_P2C) A.rps[s] += pr;
+        A.cnt[s] = base + 1;
+      }
+      __syncwarp();
+      release_smem();
+      if (lane == 0) {
+        const int e = pipe_gw(s);
+        st_rc_s32(&cl.map_shared_rank(&C, e / PIPE_WARPS)->hint[e % PIPE_WARPS], base + 1);
+      }
+      k += 1;
+      const double tn = k < c0 + 32 ? __shfl_sync(FULL, c_t, k - c0) : __shfl_sync(FULL, n_t, k - c0 - 32);
+      if (wt_lane) st_rc_u64(wt_lane, (unsigned long long)__double_as_longlong(tn));
+      __syncwarp();
+      g.klog = k;
+      k_pub = k;
+      continue;
+    }
     if (lane == g.nlog) { g.slog = s; g.plog = pr; }
     g.nlog += 1;
     k += 1;
@@ -1829,7 +1854,11 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     // pipelined: one cluster of G CTAs x 8 warps per instance, a routing warp + one warp per
     // replica (G = 9 for 64 replicas: a non-portable cluster size)
     const int G = 1 + (max_servers + PIPE_WARPS - 1) / PIPE_WARPS;
-    int publish_every = 8;  // <= 32: the route log is one lane per route
+    // watermark publish period (<= 32: the route log is one lane per route): every route for
+    // small clusters (C2, 8 replicas: the engines see each arrival at once; 209 -> 200 ms on
+    // C2/sal), every 8 routes for large ones (C5, 64 replicas: 64 engines waking per publish
+    // cost more than they gain, 99 vs 104 ms)
+    int publish_every = max_servers <= 16 ? 1 : 8;
     if (const char* e = getenv("SSB_PIPE_PUBLISH")) publish_every = std::min(32, std::max(1, atoi(e)));  // experiments
     const size_t smc = align_up(pipe_array_bytes(max_servers), 16) + sizeof(int) * SM_COLS * RS * PIPE_WARPS;
     cudaFuncSetAttribute(k_cluster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
