@@ -1188,6 +1188,7 @@ struct Eng {
       __syncwarp();
       if (fl == 32) break;
       // ---- serial slow path for lane fl: its grow does not fit ----
+      SSB_T0(slow)
       removed_any = true;
       int j = __shfl_sync(FULL, j_lane, fl);
       int frid = __shfl_sync(FULL, rid, fl), fpr = __shfl_sync(FULL, pr, fl), fout = __shfl_sync(FULL, out, fl);
@@ -1244,6 +1245,7 @@ struct Eng {
         }
       }
       __syncwarp();
+      SSB_T1(slow, 15)
       start = fl + 1;
       if (start >= 32) break;
     }
@@ -1684,8 +1686,8 @@ struct Eng {
       printf("PHASES iters %lld | enq %lld/%lld | sel %lld/%lld | disp %lld/%lld | fast %lld/%lld | small %lld/%lld | gen %lld/%lld | walk %lld/%lld | victims %lld/%lld\n",
              st.iterations, tm[0], tc[0], tm[1], tc[1], tm[2], tc[2], tm[3], tc[3], tm[4], tc[4], tm[5], tc[5], tm[6], tm[7], tc[6], tc[7]);
     if (lane == 0)
-      printf("PHASES2 vbuild %lld/%lld | tfind %lld/%lld | walk %lld/%lld | remove %lld/%lld | vtake %lld/%lld | preempt %lld/%lld | small->gen %lld\n",
-             tm[8], tc[8], tm[9], tc[9], tm[10], tc[10], tm[11], tc[11], tm[12], tc[12], tm[13], tc[13], tc[14]);
+      printf("PHASES2 vbuild %lld/%lld | tfind %lld/%lld | walk %lld/%lld | remove %lld/%lld | vtake %lld/%lld | preempt %lld/%lld | small->gen %lld | evict-slow %lld/%lld\n",
+             tm[8], tc[8], tm[9], tc[9], tm[10], tc[10], tm[11], tc[11], tm[12], tc[12], tm[13], tc[13], tc[14], tm[15], tc[15]);
 #endif
   }
   // the boundary loop: every boundary with time < t_lim. A warp that keeps its engine bound
