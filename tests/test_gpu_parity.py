@@ -158,3 +158,20 @@ def test_gpu_cluster_above_pipeline_limit_matches_oracle():
         assert np.array_equal(st[k], ost[k]), k
     for col in ("first_token", "finish", "preempt_count", "server"):
         assert np.array_equal(getattr(rec, col), getattr(orec, col)), col
+
+
+def test_gpu_multicta_event_rings_fold_to_the_digests():
+    """Event export at scale through the pipelined cluster kernel (9..96 replicas): every
+    engine's exported (code, request id, time) stream re-folded on the host equals the device's
+    decision digest for that engine and the instance digest, which equal the reference's."""
+    from golden_util import event_digest, fold_digests
+
+    golden = load_golden("fuzz_multicta")
+    scs = S.GROUPS["fuzz_multicta"]()
+    batch = scenario_batch(scs)
+    rec, stats, evs, est = _sim().run_batch(batch, events=True, with_engines=True)
+    rows = np.concatenate([[0], np.cumsum(batch.instances["n_servers"])])
+    for i, (sc, ev) in enumerate(zip(scs, evs)):
+        ds = [event_digest([(int(e["code"]), int(e["request_id"]), float(e["time"])) for e in ev_s]) for ev_s in ev]
+        assert ds == [int(d) for d in est["digest"][rows[i]:rows[i + 1]]], sc["name"]
+        assert fold_digests(ds) == int(stats["digest"][i]) == int(golden[sc["name"]]["digest"], 16), sc["name"]
