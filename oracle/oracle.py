@@ -57,6 +57,8 @@ def load():
             ctypes.c_void_p, ctypes.c_int32, _abi.SsbTrace, _abi.SsbRecords, ctypes.c_void_p,
             ctypes.c_int32, ctypes.c_int32,
         ]
+        lib.ssb_oracle_set_trail_fast.restype = None
+        lib.ssb_oracle_set_trail_fast.argtypes = [ctypes.c_int32]
         lib.ssb_oracle_rng_integers.restype = None
         lib.ssb_oracle_rng_integers.argtypes = [ctypes.c_uint64] * 4 + [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         sizes = np.zeros(len(_abi.STRUCT_ORDER), dtype=np.int64)
@@ -114,6 +116,12 @@ def run_batch(batch, *, mode: int = 0, threads: int = 1, events: bool = False, e
                            cnt.ctypes.data, mode)
         evs.append(buf[: min(int(cnt[0]), cap)].copy())
     return rec, stats, evs
+
+
+def set_trail_fast(on: bool) -> None:
+    """Single-engine trail_plus runs (mode 1) use the indexed waiting set (select_trail_fast):
+    the same decisions, in time a 1M-request backlog allows (C3 at full size)."""
+    load().ssb_oracle_set_trail_fast(1 if on else 0)
 
 
 def rng_integers(seed_words, highs) -> np.ndarray:

@@ -95,6 +95,23 @@ static void dq_remove(Deque* d, Req* r) { /* deque.remove: first occurrence, O(l
   d->len--;
 }
 
+/* ---- trail_plus waiting set, fast mode (C3-size backlogs only; see select_trail_fast) ----
+ * The literal select_trail re-sorts the whole waiting list and visits every candidate on every
+ * step, and dispatch removes from the deque by a linear search: O(W log W + W*R) per step, which
+ * does not finish C3's 1M-request backlog. Fast mode keeps the waiting set as one list per
+ * remaining-output value (ascending id == (arrival, id) order: the trace is sorted) plus a
+ * segment tree of each list's minimum block need, and visits only admissible candidates.
+ * It makes the same decisions in the same order (tests/test_oracle_golden.py checks it against
+ * the literal path); it is enabled only for single-engine trail_plus runs by
+ * ssb_oracle_set_trail_fast(1) (tools/make_c3_golden.py). */
+typedef struct {
+  int64_t nb, size;    /* buckets (remaining 0..nb-1), tree leaves (power of two) */
+  int32_t *head, *tail, *next, *prev;
+  int32_t* tree;       /* [2*size]: leaf size+b = min need in bucket b (INT32_MAX empty) */
+} TrailFast;
+static int g_trail_fast = 0;
+void ssb_oracle_set_trail_fast(int32_t on) { g_trail_fast = on != 0; }
+
 /* ---- engine ------------------------------------------------------------- */
 typedef struct {
   ssb_engine_params p;
@@ -124,6 +141,8 @@ typedef struct {
   int64_t nplan_dec, nplan_pf;
   Req** finished_now;
   int64_t nfinished_now;
+  TrailFast* tf;      /* fast-mode trail_plus waiting set (NULL: the literal deque) */
+  Req* reqs;          /* request array (fast mode indexes it by id) */
 } Eng;
 
 static void eng_log(Eng* e, int code, const Req* r) { /* engine.py:273-274 */
@@ -210,10 +229,64 @@ static void running_remove(Eng* e, Req* r) { /* del self.running[id] */
   e->nrun--;
 }
 
+static void tf_fix_up(TrailFast* t, int64_t i) { /* restore node = min(children) above leaf i */
+  for (i >>= 1; i >= 1; i >>= 1) {
+    int32_t m = t->tree[2 * i] < t->tree[2 * i + 1] ? t->tree[2 * i] : t->tree[2 * i + 1];
+    if (t->tree[i] == m) break;
+    t->tree[i] = m;
+  }
+}
+static void tf_insert(Eng* e, Req* r) { /* into bucket output-generated, ascending id */
+  TrailFast* t = e->tf;
+  int64_t b = (int64_t)r->output - r->generated;
+  int32_t id = (int32_t)r->id;
+  int32_t after = t->tail[b];
+  if (after >= 0 && after > id) { /* a re-queued request: find its place from the head */
+    after = -1;
+    for (int32_t c = t->head[b]; c >= 0 && c < id; c = t->next[c]) after = c;
+  }
+  int32_t before = after >= 0 ? t->next[after] : t->head[b];
+  t->prev[id] = after; t->next[id] = before;
+  if (after >= 0) t->next[after] = id; else t->head[b] = id;
+  if (before >= 0) t->prev[before] = id; else t->tail[b] = id;
+  int64_t need = blocks_needed(pending_prefill(r), e->p.block_size);
+  int64_t leaf = t->size + b;
+  if (need < t->tree[leaf]) { t->tree[leaf] = (int32_t)need; tf_fix_up(t, leaf); }
+  e->waiting.len++;
+}
+static void tf_remove(Eng* e, Req* r) {
+  TrailFast* t = e->tf;
+  int64_t b = (int64_t)r->output - r->generated;
+  int32_t id = (int32_t)r->id, p = t->prev[id], n = t->next[id];
+  if (p >= 0) t->next[p] = n; else t->head[b] = n;
+  if (n >= 0) t->prev[n] = p; else t->tail[b] = p;
+  int32_t m = INT32_MAX;
+  for (int32_t c = t->head[b]; c >= 0; c = t->next[c]) {
+    int64_t need = blocks_needed(pending_prefill(&e->reqs[c]), e->p.block_size);
+    if (need < m) m = (int32_t)need;
+  }
+  int64_t leaf = t->size + b;
+  if (t->tree[leaf] != m) { t->tree[leaf] = m; tf_fix_up(t, leaf); }
+  e->waiting.len--;
+}
+/* first bucket >= b whose minimum need is <= T, or -1 */
+static int64_t tf_first(const TrailFast* t, int64_t b, int64_t T) {
+  if (b >= t->nb) return -1;
+  int64_t i = t->size + b;
+  if (t->tree[i] <= T) return b;
+  while (i > 1) {
+    if (!(i & 1) && t->tree[i + 1] <= T) { i = i + 1; break; }
+    i >>= 1;
+  }
+  if (i == 1) return -1;
+  while (i < t->size) { i = 2 * i; if (t->tree[i] > T) i++; }
+  return i - t->size < t->nb ? i - t->size : -1;
+}
+
 /* ---- engine internals (engine.py:287-412) ---- */
 static void eng_enqueue(Eng* e, Req* r) { /* :175-184 */
   r->enqueue_time = e->clock;
-  dq_push_back(&e->waiting, r);
+  if (e->tf) tf_insert(e, r); else dq_push_back(&e->waiting, r);
   eng_log(e, SSB_EV_ENQUEUE, r);
 }
 static void eng_preempt(Eng* e, Req* r, int code) { /* :368-379 */
@@ -224,13 +297,13 @@ static void eng_preempt(Eng* e, Req* r, int code) { /* :368-379 */
   r->enqueue_time = e->clock;
   r->dispatch_seq = -1;
   running_remove(e, r);
-  dq_push_front(&e->waiting, r);
+  if (e->tf) tf_insert(e, r); else dq_push_front(&e->waiting, r);
   if (code == SSB_EV_PARK) e->parks++; else e->preempts++;
   eng_log(e, code, r);
 }
 static void eng_dispatch(Eng* e, Req* r) { /* :287-298 */
   if (!pool_try_allocate(e, r, pending_prefill(r))) { e->status = SSB_E_INVARIANT; return; }
-  dq_remove(&e->waiting, r);
+  if (e->tf) tf_remove(e, r); else dq_remove(&e->waiting, r);
   r->state = ST_PREFILLING;
   r->dispatch_seq = e->next_seq++;
   if (r->preempt_count == 0 && isnan(r->first_dispatch)) r->first_dispatch = e->clock;
@@ -363,6 +436,63 @@ static void select_trail(Eng* e, uint8_t* marked /* indexed by running position 
   }
 }
 
+/* select_trail with the same decisions: candidates in (remaining, arrival, id) order, but only
+ * the admissible ones are visited. A candidate with remaining b is admissible iff
+ * need <= free + G(b), G(b) = blocks of the unmarked eligible running requests with remaining
+ * > b (exactly when the literal victim loop reaches free + gain >= need, :183-206); G is
+ * non-increasing in b, so free + G(b) bounds every candidate in buckets >= b and tf_first skips
+ * buckets whose minimum need exceeds it. Skipped candidates are never revisited (literal: each
+ * is visited once), and nothing changes between dispatches. slots < 1 skips every later
+ * candidate (nothing changes while skipping), so it ends the loop. */
+static void select_trail_fast(Eng* e, uint8_t* marked) {
+  TrailFast* t = e->tf;
+  int64_t bs = e->p.block_size, free = e->free_blocks;
+  int64_t running_count = e->nrun;
+  memset(marked, 0, (size_t)e->nrun);
+  int64_t nv = 0; /* eligible victims (:190-196), in (-remaining, -dispatch_seq) order (:197) */
+  if (e->p.c != 0.0)
+    for (int64_t i = 0; i < e->nrun; i++) {
+      Req* q = e->running[i];
+      if ((double)q->generated < e->p.c * (double)q->output) e->tmp2[nv++] = q;
+    }
+  qsort(e->tmp2, nv, sizeof(Req*), cmp_victim);
+  uint8_t* taken = marked; /* indexed by position in tmp2 here */
+  int64_t b = 0;
+  int32_t after = -1;
+  for (;;) {
+    if (open_slots(e, running_count + e->ndisp - e->npre) < 1) break; /* :179-181 */
+    int64_t g = 0;
+    for (int64_t i = 0; i < nv; i++)
+      if (!taken[i] && (int64_t)e->tmp2[i]->output - e->tmp2[i]->generated > b) g += pool_allocated_blocks(e, e->tmp2[i]);
+    int64_t T = free + g;
+    int64_t fb = tf_first(t, b, T);
+    if (fb < 0) break;
+    if (fb != b) { b = fb; after = -1; continue; } /* re-derive G at the found bucket */
+    int32_t c = after >= 0 ? t->next[after] : t->head[b];
+    int64_t need = 0;
+    for (; c >= 0; c = t->next[c]) {
+      need = blocks_needed(pending_prefill(&e->reqs[c]), bs);
+      if (need <= T) break;
+    }
+    if (c < 0) { b += 1; after = -1; continue; }
+    Req* r = &e->reqs[c];
+    if (need > free) { /* victims largest remaining first, youngest first, until it fits */
+      int64_t gain = 0;
+      for (int64_t i = 0; i < nv && free + gain < need; i++) {
+        Req* q = e->tmp2[i];
+        if (taken[i] || (int64_t)q->output - q->generated <= b) continue;
+        taken[i] = 1;
+        gain += pool_allocated_blocks(e, q);
+        e->preempt[e->npre++] = q;
+      }
+      free += gain;
+    }
+    e->dispatch[e->ndisp++] = r;
+    free -= need;
+    after = c;
+  }
+}
+
 typedef struct { Req* r; double neg_score; } LarryKey;
 static int cmp_larry(const void* a, const void* b) { /* key (-score, enqueue_time, id), :260-267 */
   const LarryKey* x = (const LarryKey*)a; const LarryKey* y = (const LarryKey*)b;
@@ -417,7 +547,7 @@ static void eng_step(Eng* e, StepScratch* sc) {
   switch (e->p.policy) {
     case SSB_POLICY_FCFS: select_fcfs(e); break;
     case SSB_POLICY_NOPREEMPT: select_nopreempt(e); break;
-    case SSB_POLICY_TRAIL_PLUS: select_trail(e, sc->marked); break;
+    case SSB_POLICY_TRAIL_PLUS: if (e->tf) select_trail_fast(e, sc->marked); else select_trail(e, sc->marked); break;
     case SSB_POLICY_LARRY: select_larry(e, sc->keys); break;
     default: e->status = SSB_E_ARG; return;
   }
@@ -609,6 +739,25 @@ int ssb_oracle_run(const ssb_instance* inst, ssb_trace trace, ssb_records rec, s
   for (int64_t s = 0; s < n; s++) {
     if (!eng_init(&engs[s], p, &sh, (int)s)) { status = SSB_E_ARG; goto out; }
     engs[s].ev = ev; engs[s].ev_cap = ev_cap; engs[s].ev_n = ev_count;
+    engs[s].reqs = reqs;
+  }
+  TrailFast tfs;
+  memset(&tfs, 0, sizeof(tfs));
+  if (g_trail_fast && mode == 1 && p->policy == SSB_POLICY_TRAIL_PLUS) {
+    int64_t maxo = 1;
+    for (int64_t i = 0; i < N; i++) if (reqs[i].output > maxo) maxo = reqs[i].output;
+    tfs.nb = maxo + 1;
+    tfs.size = 1;
+    while (tfs.size < tfs.nb) tfs.size *= 2;
+    tfs.head = (int32_t*)malloc(sizeof(int32_t) * tfs.nb);
+    tfs.tail = (int32_t*)malloc(sizeof(int32_t) * tfs.nb);
+    tfs.next = (int32_t*)malloc(sizeof(int32_t) * (N > 0 ? N : 1));
+    tfs.prev = (int32_t*)malloc(sizeof(int32_t) * (N > 0 ? N : 1));
+    tfs.tree = (int32_t*)malloc(sizeof(int32_t) * 2 * tfs.size);
+    if (!tfs.head || !tfs.tail || !tfs.next || !tfs.prev || !tfs.tree) { status = SSB_E_ARG; goto out; }
+    for (int64_t i = 0; i < tfs.nb; i++) tfs.head[i] = tfs.tail[i] = -1;
+    for (int64_t i = 0; i < 2 * tfs.size; i++) tfs.tree[i] = INT32_MAX;
+    engs[0].tf = &tfs;
   }
 
   if (mode == 1) {
@@ -753,6 +902,7 @@ int ssb_oracle_run(const ssb_instance* inst, ssb_trace trace, ssb_records rec, s
     st->digest *= FNV_PRIME;
   }
 out:
+  free(tfs.head); free(tfs.tail); free(tfs.next); free(tfs.prev); free(tfs.tree);
   for (int64_t s = 0; s < n; s++) eng_free(&engs[s]);
 out_nofree_engs:
   shared_free(&sh);

@@ -85,3 +85,30 @@ def test_event_details_rebuilt_from_device_streams(group):
             e = Engine.__new__(Engine)
             e.event_log = event_log_with_details(ev[ev["server"] == s])
             assert e.event_lines() == want[s], (sc["name"], s)
+
+
+def test_oracle_fast_trail_plus_equals_literal():
+    """The oracle's fast trail_plus waiting set (the one that writes tests/golden/c3_full.json)
+    makes the literal re-sort-every-step oracle's decisions: every single-engine trail_plus
+    scenario of the reference goldens, block sizes that are not powers of two, c in
+    {0, .25, .5, 1}, and C3's first 20,000 s (tight pool, long tails, 10^5 preemptions)."""
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200 import instances as I
+
+    scs = [s for g in ("engine_unit", "fuzz_engine", "fuzz_odd_blocks", "c3")
+           for s in S.GROUPS[g]() if s["mode"] == "engine" and s["engine"]["policy"] == "trail_plus"]
+    assert len(scs) > 50
+    batches = [scenario_batch(scs), I.make_batch(C.c3_jobs(20000.0)[1:])]
+    for batch in batches:
+        try:
+            O.set_trail_fast(False)
+            r0, s0 = O.run_batch(batch, mode=1, threads=4)
+            O.set_trail_fast(True)
+            r1, s1 = O.run_batch(batch, mode=1, threads=4)
+        finally:
+            O.set_trail_fast(False)
+        assert np.array_equal(s0, s1)
+        for col in ("first_token", "finish", "first_dispatch", "preempt_count", "server"):
+            a, b = getattr(r0, col), getattr(r1, col)
+            assert np.array_equal(a.view(np.int64) if a.dtype == np.float64 else a,
+                                  b.view(np.int64) if b.dtype == np.float64 else b), col
