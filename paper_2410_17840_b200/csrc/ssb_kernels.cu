@@ -910,8 +910,12 @@ constexpr unsigned long long SYNC_BIT = 0x8000000000000000ULL;  // watermark tim
 
 // cluster warp of server s: rank 0 is the routing warp's alone (its SM's issue slots and
 // shared-memory port serve the serial routing chain), the servers take every warp of ranks 1..
-__host__ __device__ constexpr int pipe_gw(int s) { return s + PIPE_WARPS; }
-__device__ __forceinline__ int pipe_server(int gw) { return gw >= PIPE_WARPS ? gw - PIPE_WARPS : -1; }
+// epc engine warps per CTA (4 for small clusters: fewer co-resident engines per SM; 8 for large)
+__host__ __device__ constexpr int pipe_rank(int s, int epc) { return 1 + s / epc; }
+__host__ __device__ constexpr int pipe_warp(int s, int epc) { return s % epc; }
+__device__ __forceinline__ int pipe_server(int rank, int warp, int epc) {
+  return rank >= 1 && warp < epc ? (rank - 1) * epc + warp : -1;
+}
 
 __device__ __forceinline__ void release_smem() {
   asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
@@ -993,7 +997,7 @@ struct PipeLog {  // route log: lane i holds the server / prompt of arrival klog
 // only flushed here, so every ring slot the flow control waits on was hinted before.
 template <int BAL>
 __device__ __forceinline__ void pipe_publish(PipeLog& g, PipeArrays& A, PipeCtl& C, int lane,
-                                             unsigned long long* wt_lane, unsigned long long word) {
+                                             unsigned long long* wt_lane, unsigned long long word, int epc) {
 #ifdef SSB_PIPE_PROBE
   const long long pf0 = clock64();
 #endif
@@ -1017,10 +1021,8 @@ __device__ __forceinline__ void pipe_publish(PipeLog& g, PipeArrays& A, PipeCtl&
     __syncwarp();
   }
   release_smem();  // ring slots (and abort) before their counts and the watermark
-  if (valid && lane == leader) {
-    const int e = pipe_gw(s);
-    st_rc_s32(&cl.map_shared_rank(&C, e / PIPE_WARPS)->hint[e % PIPE_WARPS], base + gsz);
-  }
+  if (valid && lane == leader)
+    st_rc_s32(&cl.map_shared_rank(&C, pipe_rank(s, epc))->hint[pipe_warp(s, epc)], base + gsz);
   if (wt_lane) st_rc_u64(wt_lane, word);
   __syncwarp();
   g.klog += g.nlog;
@@ -1033,7 +1035,7 @@ __device__ __forceinline__ void pipe_publish(PipeLog& g, PipeArrays& A, PipeCtl&
 template <int BAL, int VPL>
 __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cfg, const double* __restrict__ arr,
                                             const int* __restrict__ prm, PipeArrays A, PipeCtl& C, int G,
-                                            int publish_every) {
+                                            int publish_every, int epc) {
   cg::cluster_group cl = cg::this_cluster();
   const int lane = lane_id();
   const int n = I.n_servers;
@@ -1062,7 +1064,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
     const int q = lane + 32 * j;
     key0[j] = q < n ? (unsigned long long)q << 1 : ~0ULL;
     vq[j] = 0; vf[j] = (long long)cfg.pool * bs; vif[j] = 0;
-    snp[j] = q < n ? &cl.map_shared_rank(&C, pipe_gw(q) / PIPE_WARPS)->snap[pipe_gw(q) % PIPE_WARPS] : nullptr;
+    snp[j] = q < n ? &cl.map_shared_rank(&C, pipe_rank(q, epc))->snap[pipe_warp(q, epc)] : nullptr;
   }
   bool anybig = false;  // some queued >= 2^50: the integer key would not be exact (warp-uniform)
   double beta = isnan(I.beta_fixed) ? beta_prior : I.beta_fixed;
@@ -1104,7 +1106,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
 #ifdef SSB_PIPE_TIMELINE
       const unsigned long long tl0 = globaltimer_ns();
 #endif
-      pipe_publish<BAL>(g, A, C, lane, wt_lane, word);
+      pipe_publish<BAL>(g, A, C, lane, wt_lane, word, epc);
       k_pub = k;
 #ifdef SSB_PIPE_PROBE
       const long long pw0 = clock64();
@@ -1290,10 +1292,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
       }
       __syncwarp();
       release_smem();
-      if (lane == 0) {
-        const int e = pipe_gw(s);
-        st_rc_s32(&cl.map_shared_rank(&C, e / PIPE_WARPS)->hint[e % PIPE_WARPS], base + 1);
-      }
+      if (lane == 0) st_rc_s32(&cl.map_shared_rank(&C, pipe_rank(s, epc))->hint[pipe_warp(s, epc)], base + 1);
       k += 1;
       const double tn = k < c0 + 32 ? __shfl_sync(FULL, c_t, k - c0) : __shfl_sync(FULL, n_t, k - c0 - 32);
       if (wt_lane) st_rc_u64(wt_lane, (unsigned long long)__double_as_longlong(tn));
@@ -1310,7 +1309,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
 #ifdef SSB_PIPE_PROBE
       const long long pp0 = clock64();
 #endif
-      pipe_publish<BAL>(g, A, C, lane, wt_lane, (unsigned long long)__double_as_longlong(tn));
+      pipe_publish<BAL>(g, A, C, lane, wt_lane, (unsigned long long)__double_as_longlong(tn), epc);
       k_pub = k;
 #ifdef SSB_PIPE_PROBE
       if (lane == 0) C.p_pub += clock64() - pp0;
@@ -1322,7 +1321,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
 #endif
   if (aborted) {
     if (lane == 0) C.abort = 1;
-    pipe_publish<BAL>(g, A, C, lane, wt_lane, (unsigned long long)__double_as_longlong(INF) | SYNC_BIT);  // wake everyone
+    pipe_publish<BAL>(g, A, C, lane, wt_lane, (unsigned long long)__double_as_longlong(INF) | SYNC_BIT, epc);  // wake everyone
   }
 }
 
@@ -1330,7 +1329,7 @@ template <int POL>
 __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst, const int* __restrict__ order,
                                           ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
                                           unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
-                                          int64_t* ev_count, long long* smem_ll, PipeCtl& C, int publish_every) {
+                                          int64_t* ev_count, long long* smem_ll, PipeCtl& C, int publish_every, int epc) {
   cg::cluster_group cl = cg::this_cluster();
   const int G = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
@@ -1341,7 +1340,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   const int n_al = (n + 1) & ~1;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int gw = rank * PIPE_WARPS + warp;
-  const int s = pipe_server(gw);  // this warp's server (-1: the router or a spare warp)
+  const int s = pipe_server(rank, warp, epc);  // this warp's server (-1: the router or a spare warp)
   PipeCtl& C0 = rank == 0 ? C : *cl.map_shared_rank(&C, 0);
   PipeArrays A(rank == 0 ? smem_ll : cl.map_shared_rank(smem_ll, 0), n_al);
   int* const tab = (int*)((unsigned char*)smem_ll + align_up(pipe_array_bytes(n), 16)) + warp * SM_COLS * RS;
@@ -1393,15 +1392,15 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
     const int* prm = tr.prompt + I.trace_offset;
     const bool v2 = n <= 64;
     switch (I.balancer) {
-      case SSB_BAL_RR: pipe_router<SSB_BAL_RR, 1>(I, cfg, arr, prm, A, C, G, 32); break;
-      case SSB_BAL_RANDOM: pipe_router<SSB_BAL_RANDOM, 1>(I, cfg, arr, prm, A, C, G, 32); break;
+      case SSB_BAL_RR: pipe_router<SSB_BAL_RR, 1>(I, cfg, arr, prm, A, C, G, 32, epc); break;
+      case SSB_BAL_RANDOM: pipe_router<SSB_BAL_RANDOM, 1>(I, cfg, arr, prm, A, C, G, 32, epc); break;
       case SSB_BAL_P2C:
-        if (v2) pipe_router<SSB_BAL_P2C, 2>(I, cfg, arr, prm, A, C, G, publish_every);
-        else pipe_router<SSB_BAL_P2C, 4>(I, cfg, arr, prm, A, C, G, publish_every);
+        if (v2) pipe_router<SSB_BAL_P2C, 2>(I, cfg, arr, prm, A, C, G, publish_every, epc);
+        else pipe_router<SSB_BAL_P2C, 4>(I, cfg, arr, prm, A, C, G, publish_every, epc);
         break;
       default:
-        if (v2) pipe_router<SSB_BAL_SAL, 2>(I, cfg, arr, prm, A, C, G, publish_every);
-        else pipe_router<SSB_BAL_SAL, 4>(I, cfg, arr, prm, A, C, G, publish_every);
+        if (v2) pipe_router<SSB_BAL_SAL, 2>(I, cfg, arr, prm, A, C, G, publish_every, epc);
+        else pipe_router<SSB_BAL_SAL, 4>(I, cfg, arr, prm, A, C, G, publish_every, epc);
         break;
     }
   } else if (engine) {
@@ -1574,15 +1573,15 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
 __global__ void __launch_bounds__(32 * PIPE_WARPS, 1)
 k_cluster_pipe(const ssb_instance* __restrict__ inst, const int* __restrict__ order, ssb_trace tr, ssb_records rec,
                ssb_stats* __restrict__ stats, unsigned char* __restrict__ scratch, ssb_event* events, long long ev_cap,
-               int64_t* ev_count, int publish_every) {
+               int64_t* ev_count, int publish_every, int epc) {
   extern __shared__ long long smem_ll[];
   __shared__ PipeCtl C;
   const int G = (int)cg::this_cluster().num_blocks();
   switch (inst[order[blockIdx.x / G]].engine.policy) {
-    case SSB_POLICY_FCFS: pipe_body<SSB_POLICY_FCFS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
-    case SSB_POLICY_NOPREEMPT: pipe_body<SSB_POLICY_NOPREEMPT>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
-    case SSB_POLICY_TRAIL_PLUS: pipe_body<SSB_POLICY_TRAIL_PLUS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
-    default: pipe_body<SSB_POLICY_LARRY>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every); break;
+    case SSB_POLICY_FCFS: pipe_body<SSB_POLICY_FCFS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
+    case SSB_POLICY_NOPREEMPT: pipe_body<SSB_POLICY_NOPREEMPT>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
+    case SSB_POLICY_TRAIL_PLUS: pipe_body<SSB_POLICY_TRAIL_PLUS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
+    default: pipe_body<SSB_POLICY_LARRY>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
   }
 }
 
@@ -1853,7 +1852,12 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
   if (!multis_done && max_servers <= PIPE_MAX_SERVERS && getenv("SSB_CLUSTER_CLASSIC") == nullptr) {
     // pipelined: one cluster of G CTAs x 8 warps per instance, a routing warp + one warp per
     // replica (G = 9 for 64 replicas: a non-portable cluster size)
-    const int G = 1 + (max_servers + PIPE_WARPS - 1) / PIPE_WARPS;
+    // engine warps per CTA: 4 when the cluster still fits 16 CTAs (small clusters, C2: two engine
+    // SMs instead of one), else 8 (C5's 64 replicas: 9 CTAs)
+    int epc = 1 + (max_servers + 3) / 4 <= PIPE_MAX_CTAS ? 4 : PIPE_WARPS;
+    if (const char* e = getenv("SSB_PIPE_EPC")) epc = std::min(PIPE_WARPS, std::max(1, atoi(e)));  // experiments
+    if (1 + (max_servers + epc - 1) / epc > PIPE_MAX_CTAS) epc = PIPE_WARPS;
+    const int G = 1 + (max_servers + epc - 1) / epc;
     // watermark publish period (<= 32: the route log is one lane per route): every route for
     // small clusters (C2, 8 replicas: the engines see each arrival at once; 209 -> 200 ms on
     // C2/sal), every 8 routes for large ones (C5, 64 replicas: 64 engines waking per publish
@@ -1883,7 +1887,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     }
     if (cudaLaunchKernelEx(&lc, k_cluster_pipe, (const ssb_instance*)d_inst, (const int*)(d_hdr + off_multi), trace,
                            records, d_stats, scratch, d_events, (long long)event_cap, (int64_t*)d_event_count,
-                           publish_every) == cudaSuccess)
+                           publish_every, epc) == cudaSuccess)
       multis_done = true;
     else
       cudaGetLastError();  // e.g. the cluster size does not fit: the classic kernel below
