@@ -20,7 +20,8 @@ from . import instances as I
 from .metrics import instance_groups
 from .simulate import DeviceBatch, SimulationError, estimate_cost, retry_overflows
 
-SUMMARY_LAUNCHES = 18  # k_init + 8 x (k_hist + k_select) + k_finish
+SUMMARY_LAUNCHES = 18  # radix path: k_init + 8 x (k_hist + k_select) + k_finish
+SMALL_GROUP_MAX = 4096  # every group this small: one k_small_summary launch (ssb_summary.cu)
 
 
 class SweepRunner:
@@ -77,7 +78,8 @@ class SweepRunner:
 
     @property
     def launches_per_run(self) -> int:
-        return self.sim_launches + SUMMARY_LAUNCHES
+        small = len(self.h_groups) > 0 and int(self.h_groups["n"].max()) <= SMALL_GROUP_MAX
+        return self.sim_launches + (1 if small else SUMMARY_LAUNCHES)
 
     def copy_inputs(self):
         for d, h in ((self.d_arrival, self.p_arrival), (self.d_prompt, self.p_prompt), (self.d_output, self.p_output),

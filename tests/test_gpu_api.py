@@ -164,3 +164,26 @@ def test_pooled_percentiles_on_device_match_sorted_union():
     want = pooled_expected(*pooled_host_values(batch, rec))
     for k, v in want.items():
         assert got[k] == v or (v != v and got[k] != got[k]), (k, got[k], v)
+
+
+def test_small_group_summary_kernel_equals_radix_path(monkeypatch):
+    """Groups of <= 4,096 records are summarised by one shared-memory sort per statistic
+    (k_small_summary); it must give the 8-pass radix select's bytes exactly (ranks, NaN/inf
+    keys, the TPOT sample, throughput) — here on a C4 seed sweep slice, factors and pools mixed."""
+    import numpy as np
+    import torch
+
+    from paper_2410_17840_b200 import configs as C
+    from paper_2410_17840_b200.sweep import SweepRunner
+
+    jobs = C.c4_jobs(seeds=[2])[::3]
+    r = SweepRunner(jobs)
+    r.run()
+    small = r.results()[1].copy()
+    monkeypatch.setenv("SSB_SUMMARY_RADIX", "1")
+    r.summarize()
+    r.read_results()
+    torch.cuda.synchronize()
+    radix = r.results()[1]
+    assert small.tobytes() == radix.tobytes()
+    assert np.isfinite(small["ttft_p99"]).all()
