@@ -66,6 +66,24 @@ __device__ __forceinline__ void element_keys(const ssb_summary_group& G, ssb_tra
   key[4] = dkey(__dsub_rn(rec.first_dispatch[r], arr));
 }
 
+// one statistic's key (element_keys' operations for that statistic only); ~0 (sorts last) for a
+// record without a TPOT (output 1)
+__device__ __forceinline__ unsigned long long stat_key(const ssb_summary_group& G, ssb_trace tr, ssb_records rec,
+                                                       long long i, int st) {
+  const long long t = G.trace_offset + i, r = G.record_offset + i;
+  if (st == 3) {
+    const int out = tr.output[t];
+    if (out <= 1) return ~0ULL;
+    return dkey(__ddiv_rn(__dsub_rn(rec.finish[r], rec.first_token[r]), (double)(out - 1)));
+  }
+  double arr = tr.arrival[t];
+  if (G.qps_factor != 1.0) arr = __ddiv_rn(arr, G.qps_factor);
+  if (st == 2) return dkey(__dsub_rn(rec.finish[r], arr));
+  if (st == 4) return dkey(__dsub_rn(rec.first_dispatch[r], arr));
+  const double ttft = __dsub_rn(rec.first_token[r], arr);
+  return st == 0 ? dkey(ttft) : dkey(__ddiv_rn(ttft, (double)tr.prompt[t]));
+}
+
 // chunk c -> (group, element range) through the prefix array cstart[]
 __device__ __forceinline__ int find_group(const long long* cstart, int n_groups, long long c) {
   int lo = 0, hi = n_groups - 1;
@@ -334,17 +352,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_summary(ssb_trace tr, s
     }
     __syncthreads();
     n_tpot = cnt[0][0];
+#pragma unroll 1
     for (int st = 0; st < 5; ++st) {
-      for (int i = tid; i < P; i += SMALL_THREADS) {
-        unsigned long long k = ~0ULL;  // padding and the records without a TPOT sort last
-        if (i < n) {
-          unsigned long long kk[5];
-          bool has_tpot;
-          element_keys(G, tr, rec, i, kk, has_tpot);
-          if (st != 3 || has_tpot) k = kk[st];
-        }
-        keys[i] = k;
-      }
+      for (int i = tid; i < P; i += SMALL_THREADS) keys[i] = i < n ? stat_key(G, tr, rec, i, st) : ~0ULL;  // padding sorts last
       __syncthreads();
       for (int size = 2; size <= P; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
