@@ -469,6 +469,69 @@ struct Eng {
     }
   }
 
+  // First bucket >= b whose minimum need is <= its EXACT threshold free + G(bucket), or -1;
+  // T_out = that threshold. A bucket found with the looser bound T of an earlier bucket and
+  // then rejected leaves T(found) as the bound for every later bucket, so the search
+  // continues from the chunk values it already holds in registers (leaf chunk and top chunk,
+  // two levels) instead of reloading them: a rejection costs a ballot and a REDUX.
+  __device__ __forceinline__ int t_find_exact(int b, int free, int V, unsigned long long vk, int vb, long long& T_out) const {
+    long long T = (long long)free + (V > 0 ? victims_gain(V, vk, vb, b) : 0);
+    if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
+    bool exact = true;  // T is b's own threshold (not a bound carried from a rejected bucket)
+    if (cfg.tg.top != 1 || V == 0) {
+      #pragma unroll 1
+      while (true) {
+        const int fb = t_find(b, (int)T);
+        if (fb < 0 || (fb == b && exact) || V == 0) { T_out = T; return fb; }
+        long long Te = (long long)free + victims_gain(V, vk, vb, fb);
+        if (Te > 0x7ffffffeLL) Te = 0x7ffffffeLL;
+        if (p.t_lv[fb] <= Te) { T_out = Te; return fb; }
+        b = fb + 1;
+        T = Te;
+        exact = false;
+      }
+    }
+    if (b >= cfg.tg.nb) return -1;
+    int c = b >> TF_SHIFT, lo = b & (TF - 1);
+    int4 v = *reinterpret_cast<const int4*>(p.t_lv + (c << TF_SHIFT) + 4 * lane);
+    const int4 u = *reinterpret_cast<const int4*>(p.t_lv + cfg.tg.off[1] + 4 * lane);
+    const int q = 4 * lane;
+    #pragma unroll 1
+    while (true) {
+      const int t = (int)T;
+      unsigned bits = (unsigned)(v.x <= t && q >= lo) | ((unsigned)(v.y <= t && q + 1 >= lo) << 1) |
+                      ((unsigned)(v.z <= t && q + 2 >= lo) << 2) | ((unsigned)(v.w <= t && q + 3 >= lo) << 3);
+      unsigned m = __ballot_sync(FULL, bits != 0u);
+      if (m == 0u) {  // nothing left in this leaf chunk: the first later chunk whose minimum is <= T
+        const int lo1 = c + 1;
+        const unsigned b1 = (unsigned)(u.x <= t && q >= lo1) | ((unsigned)(u.y <= t && q + 1 >= lo1) << 1) |
+                            ((unsigned)(u.z <= t && q + 2 >= lo1) << 2) | ((unsigned)(u.w <= t && q + 3 >= lo1) << 3);
+        const unsigned m1 = __ballot_sync(FULL, b1 != 0u);
+        if (m1 == 0u) return -1;
+        const int f1 = __ffs(m1) - 1;
+        c = 4 * f1 + __ffs(__shfl_sync(FULL, b1, f1)) - 1;
+        lo = 0;
+        v = *reinterpret_cast<const int4*>(p.t_lv + (c << TF_SHIFT) + 4 * lane);
+        bits = (unsigned)(v.x <= t) | ((unsigned)(v.y <= t) << 1) | ((unsigned)(v.z <= t) << 2) |
+               ((unsigned)(v.w <= t) << 3);
+        m = __ballot_sync(FULL, bits != 0u);  // (non-empty: a child of a node <= T is <= T)
+      }
+      const int f = __ffs(m) - 1;
+      const int e = __ffs(__shfl_sync(FULL, bits, f)) - 1;
+      const int fb = (c << TF_SHIFT) + 4 * f + e;
+      if (fb == b && exact) { T_out = T; return fb; }
+      long long Te = (long long)free + victims_gain(V, vk, vb, fb);
+      if (Te > 0x7ffffffeLL) Te = 0x7ffffffeLL;
+      const int sel = e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+      if (__shfl_sync(FULL, sel, f) <= Te) { T_out = Te; return fb; }
+      T = Te;  // rejected: T(fb) bounds every later bucket
+      exact = false;
+      b = fb + 1;
+      lo = b & (TF - 1);
+      if (lo == 0) lo = TF;  // (fb closed its chunk: continue at the top level)
+    }
+  }
+
   // set bucket b's minimum and restore "node = min of children" up the tree
   __device__ void t_set_leaf(int b, int val) {
     if (p.t_lv[b] == val) return;
@@ -875,10 +938,9 @@ struct Eng {
     int r_prev = -1, r_cur = -1;  // ... and where its list continues after the last dispatch from b
     while (true) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;  // :179-181
-      long long T = (long long)free + (V > 0 ? victims_gain(V, vk, vb, b) : 0);
-      if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
+      long long T;
       SSB_T0(tf)
-      const int fb = t_find(b, (int)T);
+      const int fb = t_find_exact(b, free, V, vk, vb, T);
       SSB_T1(tf, 9)
 #ifdef SSB_PHASE_TIMING
       tc[6] += 1;
@@ -887,11 +949,6 @@ struct Eng {
       if (fb != b) {
         b = fb;
         after = -1;
-        if (V > 0) {  // exact threshold of the found bucket
-          T = (long long)free + victims_gain(V, vk, vb, b);
-          if (T > 0x7ffffffeLL) T = 0x7ffffffeLL;
-          if (p.t_lv[b] > T) { b += 1; continue; }
-        }
       }
       SSB_T0(wk)
       // the walk resumes behind the last dispatch from this bucket (its entries before that
@@ -1596,7 +1653,7 @@ struct Eng {
   }
 
   // ---- Engine.step (engine.py:193-234) ----
-  __device__ void step() {
+  __device__ __forceinline__ void step() {
     if (!has_work()) { st.status = SSB_E_STALL; return; }
     int nd = 0, np = 0;
     bool prefix = false;
