@@ -566,14 +566,15 @@ struct Eng {
     if (need < p.t_lv[rem]) t_set_leaf(rem, need);
     st.W += 1;
   }
-  // unlink `cur` (predecessor `prev`, -1 = head; successor `nx`) from bucket b; `need` = its block need
-  __device__ void trail_remove(int b, int prev, int cur, int nx, int need) {
+  // unlink `cur` (predecessor `prev`, -1 = head; successor `nx`) from bucket b; `need` = its
+  // block need, `pmin` = the minimum need of the entries before it (select_trail walked them)
+  __device__ void trail_remove(int b, int prev, int cur, int nx, int need, int pmin) {
     __syncwarp();
     if (lane == 0) { if (prev < 0) p.t_head[b] = nx; else p.w_rid[prev] = nx; }
     __syncwarp();
-    if (need == p.t_lv[b]) {  // it may have been the minimum: recompute the bucket's
-      int mn = 0x7fffffff;
-      for (int c = p.t_head[b]; c >= 0; c = t_next(c)) mn = min(mn, blocks(t_pend(c) & 0x7fffffff));
+    if (need == p.t_lv[b] && pmin > need) {  // it was the only minimum before it: rescan the rest
+      int mn = pmin;
+      for (int c = nx; c >= 0; c = t_next(c)) mn = min(mn, blocks(t_pend(c) & 0x7fffffff));
       t_set_leaf(b, mn);
     }
     st.W -= 1;
@@ -936,6 +937,7 @@ struct Eng {
     int free = st.free_blocks;
     int b = 0, after = -1;  // resume point: bucket b, ids > after
     int r_prev = -1, r_cur = -1;  // ... and where its list continues after the last dispatch from b
+    int r_min = 0x7fffffff;  // ... and the minimum need of the entries before that point
     while (true) {
       if (cfg.max_running >= 0 && (long long)cfg.max_running - (st.R + nd - np) < 1) break;  // :179-181
       long long T;
@@ -955,7 +957,8 @@ struct Eng {
       // were not admissible then, with a larger free pool, so they are not now) instead of
       // re-walking the list from its head; next and pending of an entry are loaded together
       int prev = -1, cur = after >= 0 ? r_cur : p.t_head[b], pv = 0, need = 0, nx = -1;
-      if (after >= 0) prev = r_prev;
+      int mn = 0x7fffffff;  // minimum need of the entries before cur (carried across resumes)
+      if (after >= 0) { prev = r_prev; mn = r_min; }
       while (cur >= 0) {
 #ifdef SSB_PHASE_TIMING
         tm[6] += 1;
@@ -964,6 +967,7 @@ struct Eng {
         nx = t_next(cur);
         need = blocks(pv & 0x7fffffff);
         if ((long long)need <= T) break;
+        mn = min(mn, need);
         prev = cur;
         cur = nx;
       }
@@ -991,11 +995,12 @@ struct Eng {
       free -= need;
       __syncwarp();
       SSB_T0(rm)
-      trail_remove(b, prev, cur, nx, need);
+      trail_remove(b, prev, cur, nx, need, mn);
       SSB_T1(rm, 11)
       after = cur;
       r_prev = prev;
       r_cur = nx;
+      r_min = mn;
     }
     __syncwarp();
     nd_out = nd;
