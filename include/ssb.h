@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SSB_ABI_VERSION 2
+#define SSB_ABI_VERSION 3
 
 /* scheduler registry keys, policies.py:279 ("fcfs","nopreempt","trail_plus","larry") */
 enum { SSB_POLICY_FCFS = 0, SSB_POLICY_NOPREEMPT = 1, SSB_POLICY_TRAIL_PLUS = 2, SSB_POLICY_LARRY = 3 };
@@ -97,6 +97,16 @@ typedef struct {
    * (engine.max_tokens_per_batch above), which prebuilt engines may set differently */
   int32_t route_cap;
   int32_t _pad1;
+  /* Heterogeneous prebuilt engines (run_cluster(settings, trace, engines=[...]) with engines
+   * that differ, cluster.py:66-79): n_servers parameter sets, server s batching, allocating
+   * and costing with its own; NULL = every server uses `engine`. h_servers is the host array
+   * (read by ssb_prepare / ssb_simulate's planning), d_servers a device copy of it (read by
+   * the kernels). Every set must share engine.policy and engine.block_size (the router scales
+   * the engines' free blocks by one block size), and such an instance must fit the pipelined
+   * cluster kernel (<= 120 servers); otherwise ssb_simulate returns SSB_E_ARG. */
+  const ssb_engine_params* h_servers;
+  const ssb_engine_params* d_servers;
+  int64_t server_stride;        /* filled by ssb_prepare(): scratch bytes per server   */
 } ssb_instance;
 
 /* Running tables live in shared memory with SSB_SMEM_RUN_CAP entries per

@@ -95,7 +95,12 @@ def run_batch(batch, *, mode: int = 0, threads: int = 1, events: bool = False, e
 
     mode 0 = run_cluster heap loop; mode 1 = Engine.run (only for n_servers == 1)."""
     lib = load()
-    inst = np.ascontiguousarray(batch.instances)
+    inst = np.ascontiguousarray(batch.instances).copy()
+    keep = []  # heterogeneous prebuilt engines: per-server parameter sets (h_servers)
+    for i, srv in getattr(batch, "servers", {}).items():
+        a = np.ascontiguousarray(srv, dtype=_abi.ENGINE_PARAMS)
+        keep.append(a)
+        inst[i]["h_servers"] = a.ctypes.data
     rec = Records(batch.n_records)
     stats = np.zeros(len(inst), dtype=_abi.STATS)
     tr = _ctrace(batch.trace)

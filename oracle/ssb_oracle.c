@@ -734,10 +734,13 @@ int ssb_oracle_run(const ssb_instance* inst, ssb_trace trace, ssb_records rec, s
   }
   for (int64_t i = 0; i + 1 < N; i++)
     if (reqs[i + 1].arrival < reqs[i].arrival) { status = SSB_E_ARG; goto out_nofree_engs; } /* cluster.py:81-83 */
-  for (int64_t i = 0; i < N; i++)
-    if (!check_feasible(p, &reqs[i])) { status = SSB_E_INFEASIBLE; goto out_nofree_engs; } /* cluster.py:90-92 */
+  /* prebuilt engines that differ (cluster.py:66-79): server s with its own parameters */
+#define SERVER_PARAMS(s) (inst->h_servers ? &inst->h_servers[(s)] : p)
+  for (int64_t s = 0; s < (inst->h_servers ? n : 1); s++) /* every engine checks every request */
+    for (int64_t i = 0; i < N; i++)
+      if (!check_feasible(SERVER_PARAMS(s), &reqs[i])) { status = SSB_E_INFEASIBLE; goto out_nofree_engs; } /* cluster.py:90-92 */
   for (int64_t s = 0; s < n; s++) {
-    if (!eng_init(&engs[s], p, &sh, (int)s)) { status = SSB_E_ARG; goto out; }
+    if (!eng_init(&engs[s], SERVER_PARAMS(s), &sh, (int)s)) { status = SSB_E_ARG; goto out; }
     engs[s].ev = ev; engs[s].ev_cap = ev_cap; engs[s].ev_n = ev_count;
     engs[s].reqs = reqs;
   }

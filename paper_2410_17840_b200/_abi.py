@@ -64,6 +64,9 @@ INSTANCE = np.dtype(
         ("flags", "<i4"),
         ("route_cap", "<i4"),
         ("_pad1", "<i4"),
+        ("h_servers", "<u8"),
+        ("d_servers", "<u8"),
+        ("server_stride", "<i8"),
     ],
     align=True,
 )
@@ -155,7 +158,7 @@ STRUCT_SIZES = {
 }
 STRUCT_ORDER = ["ssb_engine_params", "ssb_instance", "ssb_stats", "ssb_event", "ssb_summary", "ssb_summary_group",
                 "ssb_engine_stats"]
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class SsbTrace(ctypes.Structure):

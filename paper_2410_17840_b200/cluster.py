@@ -129,7 +129,9 @@ def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, valida
                   resolved=None, check: bool = False) -> list[JobResult]:
     """Simulate independent instances in one launch. jobs: (settings, trace[, qps_factor[, label]]).
     check=True raises the reference's exception (StallError / RuntimeError) for the first
-    instance that did not complete, as a per-instance run_cluster call would."""
+    instance that did not complete, as a per-instance run_cluster call would.
+    resolved: per job, the ResolvedEngine of prebuilt engines, or a list of one per server
+    when they differ (each server batches, allocates and costs with its own)."""
     from . import simulate
 
     jobs = list(jobs)
@@ -137,17 +139,26 @@ def simulate_jobs(jobs, *, summaries: bool = False, events: bool = False, valida
         batch = I.make_batch(jobs, validate=validate)
     else:  # explicit ResolvedEngine per job (prebuilt engines)
         recs, traces, n_rec = [], [], 0
-        for (job, re) in zip(jobs, resolved):
+        servers = {}
+        for k, (job, re) in enumerate(zip(jobs, resolved)):
             t = as_trace(job[1])
             f = float(job[2]) if len(job) > 2 else 1.0
-            I.check_trace(t, re, f, feasibility=validate)
+            per = list(re) if isinstance(re, (list, tuple)) else None
+            if per is not None:  # every engine checks every request (cluster.py:86-88), engine order
+                for r in per:
+                    I.check_trace(t, r, f, feasibility=validate)
+                servers[k] = np.array([I.engine_params_record(r) for r in per], dtype=_abi.ENGINE_PARAMS)
+                re = per[0]
+            else:
+                I.check_trace(t, re, f, feasibility=validate)
             recs.append(I.instance_record(job[0], len(t), trace_offset=n_rec, record_offset=n_rec, qps_factor=f,
                                           resolved=re))
             traces.append(t)
             n_rec += len(t)
         tr = Trace(np.concatenate([t.arrival for t in traces]), np.concatenate([t.prompt for t in traces]),
                    np.concatenate([t.output for t in traces]))
-        batch = I.Batch(tr, np.array(recs, dtype=_abi.INSTANCE), n_rec, [j[3] if len(j) > 3 else None for j in jobs])
+        batch = I.Batch(tr, np.array(recs, dtype=_abi.INSTANCE), n_rec, [j[3] if len(j) > 3 else None for j in jobs],
+                        servers)
     db, est = simulate.simulate_batch(batch, events=events)
     rows = simulate.engine_rows(db)
     if check:
@@ -192,13 +203,14 @@ def run_cluster(settings: ClusterSettings, trace, *, engines: list[Engine] | Non
     resolved = None
     if engines is not None:
         r0 = engines[0].resolved
-        for e in engines[1:]:
-            if e.resolved != r0:
-                raise NotImplementedError("heterogeneous engines in one cluster are not supported on the device")
         for e in engines:
             if e._used:
                 raise RuntimeError("run() needs a fresh engine")
-        resolved = [r0]
+        if all(e.resolved == r0 for e in engines[1:]):
+            resolved = [r0]
+        else:  # prebuilt engines that differ: one parameter set per server
+            check_heterogeneous([e.resolved for e in engines])
+            resolved = [[e.resolved for e in engines]]
     t = as_trace(trace)
     rec_events = bool(engines) and any(e.record_events for e in engines)
     res = simulate_jobs([(settings, t, 1.0)], events=rec_events, validate=_validate, resolved=resolved)[0]
@@ -215,6 +227,21 @@ def run_cluster(settings: ClusterSettings, trace, *, engines: list[Engine] | Non
             if rec_events:
                 e.event_log = event_log_with_details(res.events[s])
     return res.records.to_records()
+
+
+def check_heterogeneous(res: list) -> None:
+    """Engines of one cluster may differ in pool size, batching limits, context window, cost
+    parameters and policy parameters; the device needs one policy kind and one block size
+    (its router scales every engine's free blocks by one block size)."""
+    from .policies import policy_descriptor
+
+    kinds = {policy_descriptor(r.policy)[0] for r in res}
+    sizes = {r.block_size for r in res}
+    if len(kinds) != 1 or len(sizes) != 1:
+        raise NotImplementedError("engines of one cluster must share the policy and the block size on the device "
+                                  f"(policies {sorted(kinds)}, block sizes {sorted(sizes)})")
+    if len(res) > 120:
+        raise NotImplementedError("heterogeneous engines: at most 120 servers (the pipelined cluster kernel)")
 
 
 def event_log_with_details(ev) -> list[tuple[str, float, int, str]]:

@@ -68,6 +68,26 @@ __host__ __device__ inline Layout make_layout(long long Wc, long long Rc, long l
   return L;
 }
 
+// Server s's parameter set: its own when the instance carries prebuilt engines that differ
+// (ssb_instance.d_servers, cluster.py:66-79), else the instance's one set.
+__device__ inline const ssb_engine_params& server_params(const ssb_instance& I, int s) {
+  return I.d_servers != nullptr ? I.d_servers[s] : I.engine;
+}
+// The instance's layout with the per-server stride ssb_prepare chose. Every field before the
+// trail tree sits at the same offset for every parameter set (only t_head / t_lv depend on
+// it), so this layout addresses any server's Srv / route list; server_layout gives server s's
+// own tree offsets under the same stride.
+__host__ __device__ inline Layout inst_layout(const ssb_instance& I) {
+  Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+  if (I.server_stride > 0) L.total = I.server_stride;
+  return L;
+}
+__device__ inline Layout server_layout(const ssb_instance& I, int s) {
+  Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, server_params(I, s));
+  if (I.server_stride > 0) L.total = I.server_stride;
+  return L;
+}
+
 // Arrival times of an instance as the engines read them: the trace itself when qps_factor is
 // 1, else the instance's scaled copy (arrival / qps_factor, workload.py:193 scale_qps) that
 // k_scale_arrivals writes into its scratch after the servers' regions — so no binary64
@@ -107,9 +127,8 @@ __device__ inline SrvPtr make_ptrs(unsigned char* base, const Layout& L) {
   return p;
 }
 
-__device__ inline Cfg make_cfg(const ssb_instance& I) {
+__device__ inline Cfg make_cfg(const ssb_instance& I, const ssb_engine_params& e) {
   Cfg c;
-  const ssb_engine_params& e = I.engine;
   c.policy = e.policy;
   c.max_output = e.max_output;
   c.bs = e.block_size;
@@ -133,6 +152,7 @@ __device__ inline Cfg make_cfg(const ssb_instance& I) {
   c.tg = trail_geom(e.max_context, e.pool_blocks, e.block_size);
   return c;
 }
+__device__ inline Cfg make_cfg(const ssb_instance& I) { return make_cfg(I, I.engine); }
 
 __device__ inline void init_srv(Srv& s, const Cfg& c) {
   s.clock = 0.0;
@@ -221,7 +241,7 @@ __global__ void k_scale_arrivals(const ssb_instance* __restrict__ inst, int n_in
   for (int i = blockIdx.x; i < n_inst; i += gridDim.x) {
     const ssb_instance I = inst[i];
     if (I.qps_factor == 1.0) continue;
-    const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+    const Layout L = inst_layout(I);
     double* out = (double*)(scratch + scaled_arrivals_offset(I, L));
     const double* in = tr.arrival + I.trace_offset;
     for (long long k = threadIdx.x; k < I.n_requests; k += blockDim.x) out[k] = __ddiv_rn(in[k], I.qps_factor);
@@ -261,7 +281,7 @@ __device__ __forceinline__ void run_instance(const ssb_instance* __restrict__ in
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;  // compile-time policy: this copy of the engine holds only POL's code
   cfg.wide = WIDE;   // latency-mode kernel only (see k_engines)
-  const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+  const Layout L = inst_layout(I);
   Eng E;
   bind_engine(E, I, cfg, scratch, 0, L, tr, rec, events ? events + (long long)idx * ev_cap : nullptr, ev_cap, sm_tab);
   clear_records(E, I.n_requests, lane, 32);
@@ -514,9 +534,17 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
   // cluster (<= 8 replicas) uses the cheaper CTA barrier
   auto csync = [&]() { if (G == 1) __syncthreads(); else cl.sync(); };
   auto tab_of = [&](int s) { return tabs_in_smem ? sm_tabs + ((s / GW) * nwarps + warp) * SM_COLS * RS : nullptr; };
+  if (I.d_servers != nullptr) {  // one parameter set per warp's servers: heterogeneous engines need k_cluster_pipe
+    if (rank == 0 && threadIdx.x == 0) {
+      ssb_stats out = {};
+      out.status = SSB_E_ARG;
+      stats[idx] = out;
+    }
+    return;
+  }
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;
-  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
+  const Layout L = inst_layout(I);
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
 
   // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
@@ -1063,7 +1091,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
   for (int j = 0; j < VPL; ++j) {
     const int q = lane + 32 * j;
     key0[j] = q < n ? (unsigned long long)q << 1 : ~0ULL;
-    vq[j] = 0; vf[j] = (long long)cfg.pool * bs; vif[j] = 0;
+    vq[j] = 0; vf[j] = q < n ? (long long)server_params(I, q).pool_blocks * bs : 0; vif[j] = 0;
     snp[j] = q < n ? &cl.map_shared_rank(&C, pipe_rank(q, epc))->snap[pipe_warp(q, epc)] : nullptr;
   }
   bool anybig = false;  // some queued >= 2^50: the integer key would not be exact (warp-uniform)
@@ -1344,9 +1372,11 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   PipeCtl& C0 = rank == 0 ? C : *cl.map_shared_rank(&C, 0);
   PipeArrays A(rank == 0 ? smem_ll : cl.map_shared_rank(smem_ll, 0), n_al);
   int* const tab = (int*)((unsigned char*)smem_ll + align_up(pipe_array_bytes(n), 16)) + warp * SM_COLS * RS;
-  Cfg cfg = make_cfg(I);
+  const int s_own = s >= 0 && s < n ? s : 0;  // the router / spare warps take server 0's set
+  Cfg cfg = make_cfg(I, server_params(I, s_own));  // each replica with its own engine parameters
   cfg.policy = POL;
-  const Layout L = make_layout(I.wait_cap, I.run_cap, N, n, I.engine);
+  const Layout L = inst_layout(I);
+  const Layout Ls = server_layout(I, s_own);  // its own trail tree offsets
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
   const double INF = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -1373,7 +1403,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
   Eng E;
   const bool engine = s >= 0 && s < n;
   if (engine) {
-    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab);
+    bind_engine(E, I, cfg, scratch, s, Ls, tr, rec, evb, ev_cap, tab);
     init_srv(E.st, cfg);
     if (POL == SSB_POLICY_TRAIL_PLUS) E.trail_init();
     fill_events(E, lane, 32);
@@ -1626,7 +1656,7 @@ __global__ void k_engine_stats(const ssb_instance* __restrict__ inst, int n_inst
       __syncthreads();
       continue;
     }
-    const Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+    const Layout L = inst_layout(I);
     for (int s = threadIdx.x; s < I.n_servers; s += blockDim.x) {
       const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
       ssb_engine_stats e;
@@ -1703,14 +1733,23 @@ extern "C" size_t ssb_prepare(ssb_instance* h, int32_t n_inst) {
     ssb_instance& I = h[i];
     long long N = I.n_requests;
     long long Wc = std::max(1LL, N);
-    long long Rc = std::min<long long>(I.engine.pool_blocks, N);
-    if (I.engine.max_running > 0) Rc = std::min<long long>(Rc, I.engine.max_running);
-    Rc = std::max(1LL, Rc);
+    // heterogeneous prebuilt engines: tables sized for the largest server, one stride for all
+    const int n_sets = I.h_servers != nullptr ? std::max(1, I.n_servers) : 1;
+    long long Rc = 1;
+    for (int s = 0; s < n_sets; ++s) {
+      const ssb_engine_params& e = I.h_servers != nullptr ? I.h_servers[s] : I.engine;
+      long long r = std::min<long long>(e.pool_blocks, N);
+      if (e.max_running > 0) r = std::min<long long>(r, e.max_running);
+      Rc = std::max(Rc, r);
+    }
     I.wait_cap = (int32_t)Wc;
     I.run_cap = (int32_t)Rc;
     I.scratch_offset = off;
-    Layout L = make_layout(Wc, Rc, N, I.n_servers, I.engine);
-    off += L.total * (long long)std::max(1, I.n_servers);
+    long long stride = 0;
+    for (int s = 0; s < n_sets; ++s)
+      stride = std::max(stride, make_layout(Wc, Rc, N, I.n_servers, I.h_servers != nullptr ? I.h_servers[s] : I.engine).total);
+    I.server_stride = stride;
+    off += stride * (long long)std::max(1, I.n_servers);
     if (I.qps_factor != 1.0) off += align_up(8 * N, 256);  // scaled arrival times
   }
   return (size_t)off;
@@ -1731,15 +1770,23 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const ssb_instance& I = h_inst[i];
     if (I.n_servers < 1 || I.n_requests < 0 || I.n_requests > 0x7fffffffLL || I.wait_cap < 1 || I.run_cap < 1)
       return SSB_E_ARG;
-    if (I.engine.block_size < 1 ||
-        ((long long)I.engine.max_context + I.engine.block_size) * I.engine.block_size >= (1LL << 32))
-      return SSB_E_ARG;  // blocks(): multiply-shift division exact for token counts < 2^32 / block_size
-    if (I.engine.policy == SSB_POLICY_LARRY && I.engine.max_context >= (1 << 22))
-      return SSB_E_ARG;  // larry_score: queue_len * pending < 2^31 * 2^22 is exact in binary64
-    if (I.engine.policy == SSB_POLICY_TRAIL_PLUS &&
-        std::min<long long>(I.engine.max_context, (long long)I.engine.pool_blocks * I.engine.block_size) >= (1LL << 20))
-      return SSB_E_ARG;  // remaining-output buckets: 3 tree levels (2^20 buckets) at most
-    Layout L = make_layout(I.wait_cap, I.run_cap, I.n_requests, I.n_servers, I.engine);
+    if (I.h_servers != nullptr) {  // heterogeneous engines: one policy and block size, pipelined kernel
+      if (I.d_servers == nullptr || I.n_servers < 2 || I.n_servers > PIPE_MAX_SERVERS) return SSB_E_ARG;
+      if (I.server_stride < inst_layout(I).total) return SSB_E_ARG;  // not prepared
+    }
+    const int n_sets = I.h_servers != nullptr ? I.n_servers : 1;
+    for (int s = 0; s < n_sets; ++s) {
+      const ssb_engine_params& e = I.h_servers != nullptr ? I.h_servers[s] : I.engine;
+      if (e.policy != I.engine.policy || e.block_size != I.engine.block_size) return SSB_E_ARG;
+      if (e.block_size < 1 || ((long long)e.max_context + e.block_size) * e.block_size >= (1LL << 32))
+        return SSB_E_ARG;  // blocks(): multiply-shift division exact for token counts < 2^32 / block_size
+      if (e.policy == SSB_POLICY_LARRY && e.max_context >= (1 << 22))
+        return SSB_E_ARG;  // larry_score: queue_len * pending < 2^31 * 2^22 is exact in binary64
+      if (e.policy == SSB_POLICY_TRAIL_PLUS &&
+          std::min<long long>(e.max_context, (long long)e.pool_blocks * e.block_size) >= (1LL << 20))
+        return SSB_E_ARG;  // remaining-output buckets: 3 tree levels (2^20 buckets) at most
+    }
+    Layout L = inst_layout(I);
     need = std::max(need, scaled_arrivals_offset(I, L) + (I.qps_factor != 1.0 ? 8 * I.n_requests : 0));
     if (I.n_servers == 1) singles.push_back(i); else { multis.push_back(i); max_servers = std::max(max_servers, I.n_servers); }
   }

@@ -136,6 +136,9 @@ class Batch:
     instances: np.ndarray  # INSTANCE records
     n_records: int
     labels: list = field(default_factory=list)
+    # instance index -> ENGINE_PARAMS array (n_servers rows) for clusters of prebuilt engines
+    # that differ (run_cluster(..., engines=[...]), cluster.py:66-79); absent = homogeneous
+    servers: dict = field(default_factory=dict)
 
 
 def make_batch(jobs, *, validate: bool = True) -> Batch:

@@ -93,16 +93,22 @@ def _engine_key(eng):
             float(eng.cost.compute_per_token_s), float(eng.cost.overhead_s))
 
 
-def instance_row(settings, engine, n_requests: int, *, trace_offset: int = 0, record_offset: int = 0,
-                 qps_factor: float = 1.0) -> np.void:
-    """One ssb_instance from a ClusterSettings (config.py:50-55) and an Engine built from it."""
+def engine_params(engine) -> np.void:
+    """ssb_engine_params of one reference Engine (its policy, pool, limits and cost)."""
     (pid, alpha, c, max_output, bs, pool, cap, max_running, max_ctx, mb, mkv, comp, ovh) = _engine_key(engine)
-    row = np.zeros((), dtype=_abi.INSTANCE)
-    e = row["engine"]
+    e = np.zeros((), dtype=_abi.ENGINE_PARAMS)
     e["policy"], e["alpha"], e["c"], e["max_output"] = pid, alpha, c, max_output
     e["block_size"], e["pool_blocks"], e["max_tokens_per_batch"] = bs, pool, cap
     e["max_running"], e["max_context"] = max_running, max_ctx
     e["mem_base_s"], e["mem_per_kv_token_s"], e["compute_per_token_s"], e["overhead_s"] = mb, mkv, comp, ovh
+    return e
+
+
+def instance_row(settings, engine, n_requests: int, *, trace_offset: int = 0, record_offset: int = 0,
+                 qps_factor: float = 1.0) -> np.void:
+    """One ssb_instance from a ClusterSettings (config.py:50-55) and an Engine built from it."""
+    row = np.zeros((), dtype=_abi.INSTANCE)
+    row["engine"] = engine_params(engine)
     b = settings.balancer
     if b.name not in BALANCER_IDS:
         raise ValueError(f"unknown balancer {b.name!r}")
@@ -119,16 +125,21 @@ def instance_row(settings, engine, n_requests: int, *, trace_offset: int = 0, re
 class _Device:
     """Device buffers + the raw ssb_simulate / ssb_engine_stats_gather / ssb_summarize calls."""
 
-    def __init__(self, inst: np.ndarray, arr, prm, out, *, events: int = 0):
+    def __init__(self, inst: np.ndarray, arr, prm, out, *, events: int = 0, servers: np.ndarray | None = None):
         import torch
 
         if not torch.cuda.is_available():
             raise RuntimeError("libssb.so needs a CUDA device (there is no CPU fallback)")
         self.torch, self.lib = torch, _abi.load_library()
         self.inst = np.ascontiguousarray(inst)
-        self.scratch_bytes = int(self.lib.ssb_prepare(self.inst.ctypes.data, len(self.inst)))
         dev = torch.device("cuda", torch.cuda.current_device())
         to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        if servers is not None:  # instance 0's engines differ: one ssb_engine_params per server
+            self.h_servers = np.ascontiguousarray(servers, dtype=_abi.ENGINE_PARAMS)
+            self.d_servers = to(self.h_servers.view(np.uint8))
+            self.inst[0]["h_servers"] = self.h_servers.ctypes.data
+            self.inst[0]["d_servers"] = self.d_servers.data_ptr()
+        self.scratch_bytes = int(self.lib.ssb_prepare(self.inst.ctypes.data, len(self.inst)))
         self.d_arr, self.d_prm, self.d_out = to(arr), to(prm), to(out)
         n = len(arr) if len(inst) == 0 else int((inst["record_offset"] + inst["n_requests"]).max())
         self.n = n
@@ -254,13 +265,17 @@ def run_cluster(settings, trace, *, engines=None, record_events: bool = False):
         engines = [R["build_engine"](settings.engine) for _ in range(n)]
     elif len(engines) != n:
         raise ValueError(f"expected {n} engines, got {len(engines)}")
-    keys = {_engine_key(e) for e in engines}
-    if len(keys) != 1:
-        raise NotImplementedError("heterogeneous engines in one cluster are not supported on the device")
+    keys = [_engine_key(e) for e in engines]
+    servers = None
+    if len(set(keys)) != 1:  # prebuilt engines that differ: each server with its own parameters
+        if len({k[0] for k in keys}) != 1 or len({k[4] for k in keys}) != 1 or n > 120:
+            raise NotImplementedError("engines of one cluster must share the policy and the block size "
+                                      "(and number <= 120) on the device")
+        servers = np.array([engine_params(e) for e in engines], dtype=_abi.ENGINE_PARAMS)
     arr, prm, out = _trace_columns(trace)
     _validate(engines, arr, prm, out, R)
     inst = np.array([instance_row(settings, engines[0], len(arr))], dtype=_abi.INSTANCE)
-    dev = _Device(inst, arr, prm, out, events=(len(arr) * 12 + 64) * n if record_events else 0)
+    dev = _Device(inst, arr, prm, out, events=(len(arr) * 12 + 64) * n if record_events else 0, servers=servers)
     st, est = dev.run()
     _raise(int(st[0]["status"]), R)
     ft, fin, pc, srv = dev.records()

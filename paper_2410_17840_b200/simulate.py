@@ -176,6 +176,8 @@ class DeviceBatch:
     event_cap: int = 0
     d_engine_offset: object = None  # row of (instance i, server 0) in the per-engine stats
     n_engines: int = 0
+    h_servers: object = None  # per-server parameter sets of heterogeneous clusters (host, device):
+    d_servers: object = None  # the instances hold raw pointers into these, so they live with the batch
 
     def trace_c(self) -> _abi.SsbTrace:
         return _abi.SsbTrace(self.d_arrival.data_ptr(), self.d_prompt.data_ptr(), self.d_output.data_ptr())
@@ -192,6 +194,7 @@ def upload(batch: Batch, *, device=None, events: bool = False, event_cap: int | 
     h_inst = np.ascontiguousarray(batch.instances.copy())
     if len(h_inst):
         h_inst["est_cost"] = estimate_cost(batch)
+    h_srv, d_srv = attach_servers(torch, batch, h_inst, device)
     scratch_bytes = int(lib.ssb_prepare(h_inst.ctypes.data, len(h_inst)))
     n = batch.n_records
     db = DeviceBatch(
@@ -209,6 +212,8 @@ def upload(batch: Batch, *, device=None, events: bool = False, event_cap: int | 
         d_stats=torch.zeros(len(h_inst) * _abi.STATS.itemsize, dtype=torch.uint8, device=device),
         d_scratch=torch.empty(max(scratch_bytes, 256), dtype=torch.uint8, device=device),
         scratch_bytes=scratch_bytes,
+        h_servers=h_srv,
+        d_servers=d_srv,
     )
     ns = h_inst["n_servers"].astype(np.int64) if len(h_inst) else np.zeros(0, np.int64)
     db.n_engines = int(ns.sum())
@@ -222,6 +227,27 @@ def upload(batch: Batch, *, device=None, events: bool = False, event_cap: int | 
         cap = cap * int(max((int(i["n_servers"]) for i in h_inst), default=1))
         alloc_events(db, cap)
     return db
+
+
+def attach_servers(torch, batch: Batch, h_inst: np.ndarray, device):
+    """Point each heterogeneous cluster's h_servers / d_servers at its rows of one host
+    array and its device copy (returned: the caller keeps both alive)."""
+    if not batch.servers:
+        return None, None
+    idx = sorted(batch.servers)
+    rows = [np.asarray(batch.servers[i], dtype=_abi.ENGINE_PARAMS) for i in idx]
+    for i, r in zip(idx, rows):
+        if len(r) != int(h_inst[i]["n_servers"]):
+            raise ValueError(f"instance {i}: {len(r)} engine parameter sets for {int(h_inst[i]['n_servers'])} servers")
+    h_srv = np.ascontiguousarray(np.concatenate(rows))
+    d_srv = _np_to_dev(torch, h_srv.view(np.uint8), device)
+    sz = _abi.ENGINE_PARAMS.itemsize
+    off = 0
+    for i, r in zip(idx, rows):
+        h_inst[i]["h_servers"] = h_srv.ctypes.data + off * sz
+        h_inst[i]["d_servers"] = d_srv.data_ptr() + off * sz
+        off += len(r)
+    return h_srv, d_srv
 
 
 def alloc_events(db: DeviceBatch, cap: int) -> None:

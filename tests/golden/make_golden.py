@@ -108,7 +108,8 @@ def run_scenario(sc, full: bool):
                                       beta_prior=c["beta_prior"], beta_fixed=c["beta_fixed"]),
             seed=c["seed"],
         )
-        engines = [make_engine(e) for _ in range(c["n_servers"])]
+        engines = ([make_engine(x) for x in sc["engines"]] if "engines" in sc  # heterogeneous prebuilt engines
+                   else [make_engine(e) for _ in range(c["n_servers"])])
         records = run_cluster(settings, trace, engines=engines)
     wall = time.perf_counter() - t0
     ev_lists = [[(EVENT_CODES[ev], rid, t) for ev, t, rid, _ in eng.event_log] for eng in engines]

@@ -46,6 +46,15 @@ def scenario_trace(sc) -> Trace:
     return _trace_cache[key]
 
 
+def engine_resolved(e) -> I.ResolvedEngine:
+    """The prebuilt engine of one scenario engine dict (make_golden.make_engine)."""
+    return I.ResolvedEngine(
+        policy=make_policy(e["policy"], alpha=e["alpha"], c=e["c"], max_output=e["max_output"]),
+        pool_blocks=e["pool_blocks"], block_size=e["block_size"], cost=CostParams(*e["cost"]),
+        limits=EngineLimits(e["cap"], e["max_running"], e["max_context"]),
+    )
+
+
 def scenario_settings(sc) -> tuple[ClusterSettings, I.ResolvedEngine]:
     e, c = sc["engine"], sc["cluster"]
     es = EngineSettings(policy=e["policy"], alpha=e["alpha"], c=e["c"], max_output=e["max_output"],
@@ -68,8 +77,12 @@ def scenario_settings(sc) -> tuple[ClusterSettings, I.ResolvedEngine]:
 
 def scenario_batch(scs) -> I.Batch:
     traces, recs, toffs = [], [], {}
+    servers = {}  # heterogeneous prebuilt engines: one parameter set per server
     n_trace = n_rec = 0
-    for sc in scs:
+    for k, sc in enumerate(scs):
+        if "engines" in sc:
+            servers[k] = np.array([I.engine_params_record(engine_resolved(x)) for x in sc["engines"]],
+                                  dtype=I._abi.ENGINE_PARAMS)
         t = scenario_trace(sc)
         key = id(t)
         if key not in toffs:
@@ -82,7 +95,7 @@ def scenario_batch(scs) -> I.Batch:
         n_rec += len(t)
     tr = Trace(np.concatenate([t.arrival for t in traces]), np.concatenate([t.prompt for t in traces]),
                np.concatenate([t.output for t in traces]))
-    return I.Batch(tr, np.array(recs, dtype=I._abi.INSTANCE), n_rec, [sc["name"] for sc in scs])
+    return I.Batch(tr, np.array(recs, dtype=I._abi.INSTANCE), n_rec, [sc["name"] for sc in scs], servers)
 
 
 PER_ENGINE_FIELDS = ("iterations", "request_steps", "batch_tokens", "peak_batch_tokens")

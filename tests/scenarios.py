@@ -338,6 +338,55 @@ def prebuilt_scenarios():
     return out
 
 
+def hetero_scenarios(n=48, seed=777):
+    """run_cluster(settings, trace, engines=[...]) with prebuilt engines that DIFFER
+    (cluster.py:66-79): per server its own pool size, batching cap, running limit, context
+    window, cost parameters and policy parameters (alpha / c / max_output), one policy kind
+    and one block size per cluster. Every engine checks every request (cluster.py:86-88);
+    SAL divides by the settings' cap (cluster.py:96-104); the view's free memory and each
+    engine's batching, allocation, eviction and latency are its own. Sizes 2..8 (one CTA)
+    and 9..40 (multi-CTA clusters). Scenario key "engines": one engine dict per server."""
+    rng = np.random.default_rng(seed)
+    out = []
+    bals = ["rr", "random", "p2c", "sal"]
+    pols = ["fcfs", "nopreempt", "trail_plus", "larry"]
+    costs = [COST_A100_8B, COST_H100_70B, [2.0e-2, 1.2e-7, 2.0e-4, 1e-3]]
+    for i in range(n):
+        b = bals[i % 4]
+        pol = pols[(i // 4) % 4]
+        ns = int(rng.integers(2, 9)) if i < n // 2 else int(rng.choice([9, 16, 24, 40]))
+        nreq = int(rng.integers(40, 400 if ns <= 8 else 900))
+        arrivals = np.sort(rng.exponential(float(rng.choice([0.002, 0.02, 0.1])), nreq).cumsum())
+        bs = int(rng.choice([4, 16]))
+        prompts = rng.integers(1, int(rng.choice([64, 600, 2000])) + 1, nreq)
+        max_out = int(rng.choice([8, 60, 300]))
+        outputs = rng.integers(1, max_out + 1, nreq)
+        ctx = 8192
+        peak = max(-(-(int(p) + int(o)) // bs) for p, o in zip(prompts, outputs))
+        engs = []
+        for s in range(ns):
+            mo = max_out + int(rng.integers(0, 64)) if pol == "nopreempt" else max_out
+            need = peak
+            if pol == "nopreempt":
+                need = max(need, max(-(-min(ctx, int(p) + mo) // bs) for p in prompts))
+            pool = need + int(rng.integers(0, int(rng.choice([4, 40, 400, 4000]))))
+            mr = None if rng.random() < 0.7 else int(rng.integers(2, 64))
+            engs.append(engine(pol, alpha=float(rng.choice([0.5, 1.0, 2.0])),
+                               c=float(rng.choice([0.0, 0.25, 0.5, 1.0])) if pol == "trail_plus" else 0.0,
+                               max_output=mo, pool_blocks=pool, block_size=bs,
+                               cost=costs[int(rng.integers(0, len(costs)))],
+                               cap=int(rng.choice([32, 100, 256, 1024, 4096])), max_running=mr, max_context=ctx))
+        tr = [(float(a), int(p), int(o)) for a, p, o in zip(arrivals, prompts, outputs)]
+        sc = scen(f"hetero_{b}_{pol}_{ns}_{i}", engs[0], rows(tr), mode="cluster",
+                  clus=dict(cluster(ns, b, poll_interval_s=float(rng.choice([0.001, 0.05, 0.5, float("inf")])),
+                                    beta_fixed=None if rng.random() < 0.6 else float(rng.choice([1.0, 2.0, 6.5])),
+                                    seed=int(rng.integers(0, 1000))),
+                            route_cap=int(rng.choice([100, 512, 1024]))))
+        sc["engines"] = engs
+        out.append(sc)
+    return out
+
+
 GROUPS = {
     "engine_unit": engine_unit_scenarios,
     "c6": c6_scenarios,
@@ -359,6 +408,7 @@ GROUPS = {
                                                     nreq_range=(60, 700))
     + fuzz_cluster_scenarios(32, seed=6565, prefix="mcta_big", servers=(65, 96), nreq_range=(100, 900)),
     "prebuilt": prebuilt_scenarios,
+    "hetero": hetero_scenarios,
     "fuzz_route": lambda: fuzz_cluster_scenarios(48, seed=5151, block_sizes=(4, 16), prefix="route",
                                                  caps=(48, 100, 1000, 1024), betas=(1.0, 1.25, 9.0),
                                                  bals=("sal", "sal", "p2c")),

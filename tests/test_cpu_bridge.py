@@ -47,13 +47,14 @@ class OracleDevice:
     calls = []
     force_status = 0
 
-    def __init__(self, inst, arr, prm, out, *, events=0):
+    def __init__(self, inst, arr, prm, out, *, events=0, servers=None):
         from paper_2410_17840_b200.instances import Batch
         from paper_2410_17840_b200.workload import Trace
 
         OracleDevice.calls.append(len(inst))
         self.inst = np.ascontiguousarray(inst)
-        self.batch = Batch(Trace(arr, prm, out), self.inst, int((inst["record_offset"] + inst["n_requests"]).max()))
+        self.batch = Batch(Trace(arr, prm, out), self.inst, int((inst["record_offset"] + inst["n_requests"]).max()),
+                           servers={} if servers is None else {0: servers})
 
     def run(self):
         self.rec, st = O.run_batch(self.batch)
@@ -134,3 +135,31 @@ def test_exit_code_2_without_a_cuda_device(cfg, tmp_path, capsys):
         pytest.skip("CUDA present")
     rc = B.cli_main(["sweep", "--backend", "b200", "--config", str(cfg), "--out-dir", str(tmp_path / "o")])
     assert rc == 2 and "CUDA" in capsys.readouterr().err
+
+
+def test_heterogeneous_prebuilt_engines_route_per_server(oracle_device):
+    """run_cluster(settings, trace, engines=[...]) with the reference's own engines that differ
+    in pool, cap, running limit and cost (cluster.py:66-79): the binding hands one parameter set
+    per server to the device (here the oracle) and the records equal the reference's run; mixed
+    policy kinds are refused before any device call."""
+    from servesim.cluster import build_engine, run_cluster
+    from servesim.config import ClusterSettings, EngineSettings
+    from servesim.workload import SynthSpec, synthesize
+
+    trace = synthesize(SynthSpec(duration_s=10.0, mean_qps=40.0, burstiness=2.0, seed=5))
+    for bal, pol in (("sal", "larry"), ("p2c", "trail_plus"), ("rr", "fcfs")):
+        settings = ClusterSettings(n_servers=3, engine=EngineSettings(policy=pol, pool_blocks=900, c=0.5))
+        settings.balancer.name = bal
+        variants = [dict(pool_blocks=900), dict(pool_blocks=600, max_tokens_per_batch=256, max_running=12),
+                    dict(pool_blocks=2500, cost={"mem_base_s": 2e-2})]
+        mk = lambda: [build_engine(EngineSettings(policy=pol, c=0.5, **v)) for v in variants]  # noqa: E731
+        want = run_cluster(settings, trace, engines=mk())
+        engines = mk()
+        got = B.run_cluster(settings, trace, engines=engines)
+        assert [(r.first_token_time, r.finish_time, r.preempt_count, r.server) for r in got] == \
+               [(r.first_token_time, r.finish_time, r.preempt_count, r.server) for r in want], (bal, pol)
+    n_calls = len(oracle_device.calls)
+    mixed = [build_engine(EngineSettings(policy=p, pool_blocks=900)) for p in ("fcfs", "larry", "fcfs")]
+    with pytest.raises(NotImplementedError):
+        B.run_cluster(settings, trace, engines=mixed)
+    assert len(oracle_device.calls) == n_calls

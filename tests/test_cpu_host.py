@@ -41,7 +41,7 @@ def test_library_exports_every_header_symbol():
 
 def test_struct_layouts_match_numpy_mirror():
     lib = _abi.load_library()
-    assert lib.ssb_abi_version() == _abi.ABI_VERSION == 2
+    assert lib.ssb_abi_version() == _abi.ABI_VERSION == 3
     assert lib.ssb_error_string(3) == b"device table capacity exceeded"
 
 
@@ -55,6 +55,37 @@ def test_prepare_plans_capacities():
     assert inst[0]["run_cap"] == 9 and inst[0]["wait_cap"] == len(tr)
     assert inst[1]["run_cap"] == len(tr)
     assert inst[1]["scratch_offset"] > inst[0]["scratch_offset"] and total > inst[1]["scratch_offset"]
+
+
+def test_prepare_plans_heterogeneous_servers():
+    """Prebuilt engines that differ (cluster.py:66-79): tables sized for the largest server,
+    one per-server stride covering every server's own trail tree."""
+    lib = _abi.load_library()
+    tr = P.synthesize(P.SynthSpec(duration_s=50, mean_qps=3, seed=1))
+    b = I.make_batch([(P.ClusterSettings(3, P.EngineSettings(policy="trail_plus", pool_blocks=100)), tr, 1.0)],
+                     validate=False)
+    homo = b.instances.copy()
+    lib.ssb_prepare(homo.ctypes.data, 1)
+    srv = np.zeros(3, dtype=_abi.ENGINE_PARAMS)
+    srv[:] = b.instances[0]["engine"]
+    srv["pool_blocks"] = [100, 400, 60]  # remaining-output trees of 1,600 / 6,400 / 960 tokens
+    srv["max_running"] = [-1, -1, 4]
+    inst = b.instances.copy()
+    inst[0]["h_servers"] = srv.ctypes.data
+    total = lib.ssb_prepare(inst.ctypes.data, 1)
+    assert inst[0]["run_cap"] == min(400, len(tr)) and inst[0]["server_stride"] > homo[0]["server_stride"]
+    assert total >= inst[0]["scratch_offset"] + 3 * inst[0]["server_stride"]
+
+
+def test_heterogeneous_engines_need_one_policy_and_block_size():
+    """Mixed policy kinds or block sizes in one cluster are refused before any device work."""
+    tr = P.synthesize(P.SynthSpec(duration_s=5, mean_qps=3, seed=1))
+    cs = P.ClusterSettings(2, P.EngineSettings())
+    mk = lambda pol, bs: P.Engine(P.KvBlockPool(2000, bs), P.make_policy(pol), P.default_params("llama3-8b", "a100"),  # noqa: E731
+                                  block_size=bs)
+    for a, b in (((("fcfs", 16)), ("larry", 16)), (("fcfs", 16), ("fcfs", 8))):
+        with pytest.raises(NotImplementedError):
+            P.run_cluster(cs, tr, engines=[mk(*a), mk(*b)])
 
 
 def test_synthesize_is_bit_identical_to_reference():

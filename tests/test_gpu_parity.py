@@ -12,7 +12,7 @@ from helpers import compare_instance, load_golden, scenario_batch
 pytestmark = pytest.mark.gpu
 
 GROUPS = ["engine_unit", "cluster_unit", "c2", "c3", "c6", "fuzz_engine", "fuzz_cluster", "fuzz_odd_blocks", "fuzz_route",
-          "fuzz_multicta", "prebuilt"]
+          "fuzz_multicta", "prebuilt", "hetero"]
 
 
 def _sim():
@@ -175,3 +175,55 @@ def test_gpu_multicta_event_rings_fold_to_the_digests():
         ds = [event_digest([(int(e["code"]), int(e["request_id"]), float(e["time"])) for e in ev_s]) for ev_s in ev]
         assert ds == [int(d) for d in est["digest"][rows[i]:rows[i + 1]]], sc["name"]
         assert fold_digests(ds) == int(stats["digest"][i]) == int(golden[sc["name"]]["digest"], 16), sc["name"]
+
+
+def test_gpu_heterogeneous_engines_public_api():
+    """run_cluster(settings, trace, engines=[...]) with prebuilt engines that differ
+    (cluster.py:66-79), through the public API one call per cluster: records, every engine's
+    iterations / request-steps / batch tokens / peak batch (engine.py:225-226) and the
+    event_lines() digest equal the reference's."""
+    import paper_2410_17840_b200 as P
+    from golden_util import EVENT_CODES, event_digest, fold_digests, records_sha
+    from helpers import engine_resolved, scenario_settings, scenario_trace
+
+    golden = load_golden("hetero")
+    for sc in S.GROUPS["hetero"]()[::6]:
+        g = golden[sc["name"]]
+        cs, _ = scenario_settings(sc)
+        engines = []
+        for x in sc["engines"]:
+            re = engine_resolved(x)
+            engines.append(P.Engine(P.KvBlockPool(re.pool_blocks, re.block_size), re.policy, re.cost,
+                                    max_tokens_per_batch=re.limits.max_tokens_per_batch,
+                                    max_running=re.limits.max_running, max_context=re.limits.max_context,
+                                    record_events=True))
+        recs = P.run_cluster(cs, scenario_trace(sc), engines=engines)
+        assert records_sha([r.first_token_time for r in recs], [r.finish_time for r in recs],
+                           [r.preempt_count for r in recs], [r.server for r in recs]) == g["records_sha"], sc["name"]
+        assert [[e.iterations, e.request_steps, e.batch_tokens, e.peak_batch_tokens] for e in engines] == g["per_engine"]
+        ds = [event_digest([(EVENT_CODES[ev], rid, t) for ev, t, rid, _ in e.event_log]) for e in engines]
+        assert "%016x" % fold_digests(ds) == g["digest"], sc["name"]
+
+
+def test_gpu_heterogeneous_engines_reference_binding():
+    """The reference-side binding (servesim_bridge.run_cluster) with differing prebuilt engines."""
+    import paper_2410_17840_b200 as P
+    from golden_util import records_sha
+    from helpers import engine_resolved, scenario_settings, scenario_trace
+
+    from paper_2410_17840_b200 import servesim_bridge as B
+
+    golden = load_golden("hetero")
+    for sc in S.GROUPS["hetero"]()[1::8]:
+        g = golden[sc["name"]]
+        cs, _ = scenario_settings(sc)
+        engines = []
+        for x in sc["engines"]:
+            re = engine_resolved(x)
+            engines.append(P.Engine(P.KvBlockPool(re.pool_blocks, re.block_size), re.policy, re.cost,
+                                    max_tokens_per_batch=re.limits.max_tokens_per_batch,
+                                    max_running=re.limits.max_running, max_context=re.limits.max_context))
+        recs = B.run_cluster(cs, scenario_trace(sc).entries(), engines=engines)
+        assert records_sha([r.first_token_time for r in recs], [r.finish_time for r in recs],
+                           [r.preempt_count for r in recs], [r.server for r in recs]) == g["records_sha"], sc["name"]
+        assert [[e.iterations, e.peak_batch_tokens] for e in engines] == [[p[0], p[3]] for p in g["per_engine"]]

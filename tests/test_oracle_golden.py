@@ -9,7 +9,7 @@ from helpers import compare_instance, load_golden, scenario_batch
 from oracle import oracle as O
 
 GROUPS_FAST = ["engine_unit", "cluster_unit", "c2", "c3", "fuzz_engine", "fuzz_cluster", "c6", "fuzz_odd_blocks", "fuzz_route",
-               "fuzz_multicta", "prebuilt"]
+               "fuzz_multicta", "prebuilt", "hetero"]
 
 
 @pytest.fixture(scope="module", autouse=True)
