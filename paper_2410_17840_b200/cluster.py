@@ -230,16 +230,14 @@ def run_cluster(settings: ClusterSettings, trace, *, engines: list[Engine] | Non
 
 
 def check_heterogeneous(res: list) -> None:
-    """Engines of one cluster may differ in pool size, batching limits, context window, cost
-    parameters and policy parameters; the device needs one policy kind and one block size
-    (its router scales every engine's free blocks by one block size)."""
+    """Engines of one cluster may differ in pool size, block size, batching limits, context
+    window, cost parameters and policy parameters; the device needs one policy kind per
+    cluster (the engine code is compiled per policy for the whole thread-block cluster)."""
     from .policies import policy_descriptor
 
     kinds = {policy_descriptor(r.policy)[0] for r in res}
-    sizes = {r.block_size for r in res}
-    if len(kinds) != 1 or len(sizes) != 1:
-        raise NotImplementedError("engines of one cluster must share the policy and the block size on the device "
-                                  f"(policies {sorted(kinds)}, block sizes {sorted(sizes)})")
+    if len(kinds) != 1:
+        raise NotImplementedError(f"engines of one cluster must share the policy kind on the device (got {sorted(kinds)})")
     if len(res) > 120:
         raise NotImplementedError("heterogeneous engines: at most 120 servers (the pipelined cluster kernel)")
 

@@ -1085,13 +1085,14 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
   // server among ties; ~0 for lanes past n), free memory, in-flight; where each snapshot lives
   unsigned long long key0[VPL];
   long long vq[VPL], vf[VPL];
-  int vif[VPL];
+  int vif[VPL], bsj[VPL];  // bsj: each server's own block size (prebuilt engines may differ)
   const PipeSnap* snp[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int q = lane + 32 * j;
     key0[j] = q < n ? (unsigned long long)q << 1 : ~0ULL;
-    vq[j] = 0; vf[j] = q < n ? (long long)server_params(I, q).pool_blocks * bs : 0; vif[j] = 0;
+    bsj[j] = q < n ? server_params(I, q).block_size : bs;
+    vq[j] = 0; vf[j] = q < n ? (long long)server_params(I, q).pool_blocks * bsj[j] : 0; vif[j] = 0;
     snp[j] = q < n ? &cl.map_shared_rank(&C, pipe_rank(q, epc))->snap[pipe_warp(q, epc)] : nullptr;
   }
   bool anybig = false;  // some queued >= 2^50: the integer key would not be exact (warp-uniform)
@@ -1207,7 +1208,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
             vq[j] = wp + (A.rps[q] - en);
             key0[j] = ((unsigned long long)vq[j] << 13) | ((unsigned)q << 1);
             big |= vq[j] >= (1LL << 50);
-            vf[j] = (long long)fb * bs;
+            vf[j] = (long long)fb * bsj[j];  // snapshot_stats: free_blocks * block_size (cluster.py:54)
             vif[j] = wr + (A.cnt[q] - nx);
           }
         anybig = __any_sync(FULL, big);
@@ -1777,7 +1778,7 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const int n_sets = I.h_servers != nullptr ? I.n_servers : 1;
     for (int s = 0; s < n_sets; ++s) {
       const ssb_engine_params& e = I.h_servers != nullptr ? I.h_servers[s] : I.engine;
-      if (e.policy != I.engine.policy || e.block_size != I.engine.block_size) return SSB_E_ARG;
+      if (e.policy != I.engine.policy) return SSB_E_ARG;
       if (e.block_size < 1 || ((long long)e.max_context + e.block_size) * e.block_size >= (1LL << 32))
         return SSB_E_ARG;  // blocks(): multiply-shift division exact for token counts < 2^32 / block_size
       if (e.policy == SSB_POLICY_LARRY && e.max_context >= (1 << 22))

@@ -341,8 +341,8 @@ def prebuilt_scenarios():
 def hetero_scenarios(n=48, seed=777):
     """run_cluster(settings, trace, engines=[...]) with prebuilt engines that DIFFER
     (cluster.py:66-79): per server its own pool size, batching cap, running limit, context
-    window, cost parameters and policy parameters (alpha / c / max_output), one policy kind
-    and one block size per cluster. Every engine checks every request (cluster.py:86-88);
+    window, cost parameters, policy parameters (alpha / c / max_output) and (a third of the
+    clusters) block size, one policy kind per cluster. Every engine checks every request (cluster.py:86-88);
     SAL divides by the settings' cap (cluster.py:96-104); the view's free memory and each
     engine's batching, allocation, eviction and latency are its own. Sizes 2..8 (one CTA)
     and 9..40 (multi-CTA clusters). Scenario key "engines": one engine dict per server."""
@@ -357,14 +357,16 @@ def hetero_scenarios(n=48, seed=777):
         ns = int(rng.integers(2, 9)) if i < n // 2 else int(rng.choice([9, 16, 24, 40]))
         nreq = int(rng.integers(40, 400 if ns <= 8 else 900))
         arrivals = np.sort(rng.exponential(float(rng.choice([0.002, 0.02, 0.1])), nreq).cumsum())
-        bs = int(rng.choice([4, 16]))
+        mixed = i % 3 == 0  # a third of the clusters mix block sizes
+        bs0 = int(rng.choice([4, 16]))
         prompts = rng.integers(1, int(rng.choice([64, 600, 2000])) + 1, nreq)
         max_out = int(rng.choice([8, 60, 300]))
         outputs = rng.integers(1, max_out + 1, nreq)
         ctx = 8192
-        peak = max(-(-(int(p) + int(o)) // bs) for p, o in zip(prompts, outputs))
         engs = []
         for s in range(ns):
+            bs = int(rng.choice([4, 10, 16, 32])) if mixed else bs0
+            peak = max(-(-(int(p) + int(o)) // bs) for p, o in zip(prompts, outputs))
             mo = max_out + int(rng.integers(0, 64)) if pol == "nopreempt" else max_out
             need = peak
             if pol == "nopreempt":
