@@ -194,7 +194,11 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
             fk = (tr[0], bs[2])
             if fk not in feasible:
                 re, t = bs[0], traces[tr[0]]
-                re.policy.check_feasible_many(t.prompt, t.output, re.block_size, re.pool_blocks, re.limits)
+                if len(tr) == 3:  # the trace's maxima, once: most (trace, engine) pairs pass on them alone
+                    tr.append((int((t.prompt.astype(np.int64) + t.output).max()), int(t.prompt.max()),
+                               int(t.output.max())) if len(t) else None)
+                re.policy.check_feasible_many(t.prompt, t.output, re.block_size, re.pool_blocks, re.limits,
+                                              maxes=tr[3])
                 feasible.add(fk)
         if bs[1] < 0:  # the balancer's checks come after feasibility (cluster.py:90-104)
             bs[1] = len(templates)

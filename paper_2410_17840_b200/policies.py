@@ -58,8 +58,19 @@ class SchedulerPolicy:
         bad_pool = (-(-peak // block_size)) > pool_blocks
         return bad_ctx, bad_pool
 
-    def check_feasible_many(self, prompt, output, block_size, pool_blocks, limits) -> None:
-        """Raise InfeasibleRequestError for the first infeasible request (request-id order)."""
+    def feasible_by_max(self, maxes, block_size, pool_blocks, limits) -> bool:
+        """Every request is feasible, decided from the trace's maxima alone (max prompt +
+        output, max prompt, max output): each check of policies.py:56-68,119-131 is monotone
+        in the request's lengths, so the largest one passing means all pass. False = run the
+        per-request check (which names the first failing request)."""
+        peak, _, _ = maxes
+        return peak <= limits.max_context and -(-peak // block_size) <= pool_blocks
+
+    def check_feasible_many(self, prompt, output, block_size, pool_blocks, limits, maxes=None) -> None:
+        """Raise InfeasibleRequestError for the first infeasible request (request-id order).
+        maxes: (max prompt+output, max prompt, max output) of the trace, when known."""
+        if maxes is not None and self.feasible_by_max(maxes, block_size, pool_blocks, limits):
+            return
         masks = self._infeasible_mask(np.asarray(prompt), np.asarray(output), block_size, pool_blocks, limits)
         any_bad = np.zeros(len(prompt), dtype=bool)
         for m in masks:
@@ -110,6 +121,12 @@ class NoPreemptPolicy(SchedulerPolicy):
         a, b = super()._infeasible_mask(prompt, output, block_size, pool_blocks, limits)
         res = np.minimum(limits.max_context, prompt.astype(np.int64) + self.max_output)
         return a, b, output > self.max_output, (-(-res // block_size)) > pool_blocks
+
+    def feasible_by_max(self, maxes, block_size, pool_blocks, limits) -> bool:
+        _, pmax, omax = maxes
+        res = min(limits.max_context, pmax + self.max_output)
+        return (super().feasible_by_max(maxes, block_size, pool_blocks, limits) and omax <= self.max_output
+                and -(-res // block_size) <= pool_blocks)
 
     def check_feasible_one(self, rid, prompt, output, block_size, pool_blocks, limits) -> None:
         super().check_feasible_one(rid, prompt, output, block_size, pool_blocks, limits)

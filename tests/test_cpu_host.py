@@ -136,6 +136,25 @@ def test_feasibility_errors_match_reference_messages():
         I.check_trace(P.Trace([1.0, 0.5], [10, 10], [1, 1]), I.resolve_engine(P.EngineSettings()))
 
 
+def test_feasibility_from_trace_maxima_is_exact():
+    """make_batch decides a (trace, engine) pair from the trace's maxima when they pass; that
+    shortcut says feasible exactly when the per-request masks find nothing (monotone checks)."""
+    rng = np.random.default_rng(9)
+    for _ in range(400):
+        n = int(rng.integers(1, 40))
+        prompt = rng.integers(1, 3000, n).astype(np.int32)
+        output = rng.integers(1, 3000, n).astype(np.int32)
+        pol = P.make_policy(str(rng.choice(["fcfs", "nopreempt", "trail_plus", "larry"])),
+                            max_output=int(rng.integers(1, 4000)))
+        lim = P.EngineLimits(1024, None, int(rng.integers(500, 8192)))
+        bsz, pool = int(rng.choice([1, 3, 16])), int(rng.integers(10, 800))
+        maxes = (int((prompt.astype(np.int64) + output).max()), int(prompt.max()), int(output.max()))
+        bad = np.zeros(n, bool)
+        for m in pol._infeasible_mask(prompt, output, bsz, pool, lim):
+            bad |= m
+        assert pol.feasible_by_max(maxes, bsz, pool, lim) == (not bad.any())
+
+
 def test_custom_python_policies_are_rejected():
     class MyPolicy(P.FcfsPolicy):
         pass
