@@ -101,9 +101,9 @@ typedef struct {
    * that differ, cluster.py:66-79): n_servers parameter sets, server s batching, allocating
    * and costing with its own; NULL = every server uses `engine`. h_servers is the host array
    * (read by ssb_prepare / ssb_simulate's planning), d_servers a device copy of it (read by
-   * the kernels). Every set must share engine.policy (the engine code is compiled per policy
-   * for the whole cluster), and such an instance must fit the pipelined cluster kernel
-   * (2..120 servers); otherwise ssb_simulate returns SSB_E_ARG. */
+   * the kernels), policy included (each engine warp runs its own server's policy). Such an
+   * instance must fit the pipelined cluster kernel (2..120 servers); otherwise ssb_simulate
+   * returns SSB_E_ARG. */
   const ssb_engine_params* h_servers;
   const ssb_engine_params* d_servers;
   int64_t server_stride;        /* filled by ssb_prepare(): scratch bytes per server   */

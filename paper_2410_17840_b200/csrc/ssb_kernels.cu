@@ -1608,7 +1608,15 @@ k_cluster_pipe(const ssb_instance* __restrict__ inst, const int* __restrict__ or
   extern __shared__ long long smem_ll[];
   __shared__ PipeCtl C;
   const int G = (int)cg::this_cluster().num_blocks();
-  switch (inst[order[blockIdx.x / G]].engine.policy) {
+  const ssb_instance* const Ip = inst + order[blockIdx.x / G];
+  int pol = Ip->engine.policy;
+  if (Ip->d_servers != nullptr) {  // prebuilt engines that differ: each engine warp runs its own server's
+    // policy (a warp-uniform choice; every instantiation passes the same two cluster barriers and
+    // talks to the router through the same shared-memory protocol); the router takes server 0's
+    const int s = pipe_server((int)cg::this_cluster().block_rank(), threadIdx.x >> 5, epc);
+    if (s >= 0 && s < Ip->n_servers) pol = Ip->d_servers[s].policy;
+  }
+  switch (pol) {
     case SSB_POLICY_FCFS: pipe_body<SSB_POLICY_FCFS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
     case SSB_POLICY_NOPREEMPT: pipe_body<SSB_POLICY_NOPREEMPT>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
     case SSB_POLICY_TRAIL_PLUS: pipe_body<SSB_POLICY_TRAIL_PLUS>(inst, order, tr, rec, stats, scratch, events, ev_cap, ev_count, smem_ll, C, publish_every, epc); break;
@@ -1778,7 +1786,6 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     const int n_sets = I.h_servers != nullptr ? I.n_servers : 1;
     for (int s = 0; s < n_sets; ++s) {
       const ssb_engine_params& e = I.h_servers != nullptr ? I.h_servers[s] : I.engine;
-      if (e.policy != I.engine.policy) return SSB_E_ARG;
       if (e.block_size < 1 || ((long long)e.max_context + e.block_size) * e.block_size >= (1LL << 32))
         return SSB_E_ARG;  // blocks(): multiply-shift division exact for token counts < 2^32 / block_size
       if (e.policy == SSB_POLICY_LARRY && e.max_context >= (1 << 22))

@@ -341,8 +341,8 @@ def prebuilt_scenarios():
 def hetero_scenarios(n=48, seed=777):
     """run_cluster(settings, trace, engines=[...]) with prebuilt engines that DIFFER
     (cluster.py:66-79): per server its own pool size, batching cap, running limit, context
-    window, cost parameters, policy parameters (alpha / c / max_output) and (a third of the
-    clusters) block size, one policy kind per cluster. Every engine checks every request (cluster.py:86-88);
+    window, cost parameters, policy parameters (alpha / c / max_output), and in a third of the
+    clusters each the block size and the policy itself. Every engine checks every request (cluster.py:86-88);
     SAL divides by the settings' cap (cluster.py:96-104); the view's free memory and each
     engine's batching, allocation, eviction and latency are its own. Sizes 2..8 (one CTA)
     and 9..40 (multi-CTA clusters). Scenario key "engines": one engine dict per server."""
@@ -364,17 +364,19 @@ def hetero_scenarios(n=48, seed=777):
         outputs = rng.integers(1, max_out + 1, nreq)
         ctx = 8192
         engs = []
+        mixed_pol = i % 3 == 1  # a third of the clusters mix policies
         for s in range(ns):
             bs = int(rng.choice([4, 10, 16, 32])) if mixed else bs0
+            pol_s = str(rng.choice(pols)) if mixed_pol else pol
             peak = max(-(-(int(p) + int(o)) // bs) for p, o in zip(prompts, outputs))
-            mo = max_out + int(rng.integers(0, 64)) if pol == "nopreempt" else max_out
+            mo = max_out + int(rng.integers(0, 64)) if pol_s == "nopreempt" else max_out
             need = peak
-            if pol == "nopreempt":
+            if pol_s == "nopreempt":
                 need = max(need, max(-(-min(ctx, int(p) + mo) // bs) for p in prompts))
             pool = need + int(rng.integers(0, int(rng.choice([4, 40, 400, 4000]))))
             mr = None if rng.random() < 0.7 else int(rng.integers(2, 64))
-            engs.append(engine(pol, alpha=float(rng.choice([0.5, 1.0, 2.0])),
-                               c=float(rng.choice([0.0, 0.25, 0.5, 1.0])) if pol == "trail_plus" else 0.0,
+            engs.append(engine(pol_s, alpha=float(rng.choice([0.5, 1.0, 2.0])),
+                               c=float(rng.choice([0.0, 0.25, 0.5, 1.0])) if pol_s == "trail_plus" else 0.0,
                                max_output=mo, pool_blocks=pool, block_size=bs,
                                cost=costs[int(rng.integers(0, len(costs)))],
                                cap=int(rng.choice([32, 100, 256, 1024, 4096])), max_running=mr, max_context=ctx))

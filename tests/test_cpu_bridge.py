@@ -140,8 +140,8 @@ def test_exit_code_2_without_a_cuda_device(cfg, tmp_path, capsys):
 def test_heterogeneous_prebuilt_engines_route_per_server(oracle_device):
     """run_cluster(settings, trace, engines=[...]) with the reference's own engines that differ
     in pool, cap, running limit and cost (cluster.py:66-79): the binding hands one parameter set
-    per server to the device (here the oracle) and the records equal the reference's run; mixed
-    policy kinds are refused before any device call."""
+    per server to the device (here the oracle) and the records equal the reference's run, mixed
+    policies included."""
     from servesim.cluster import build_engine, run_cluster
     from servesim.config import ClusterSettings, EngineSettings
     from servesim.workload import SynthSpec, synthesize
@@ -158,8 +158,8 @@ def test_heterogeneous_prebuilt_engines_route_per_server(oracle_device):
         got = B.run_cluster(settings, trace, engines=engines)
         assert [(r.first_token_time, r.finish_time, r.preempt_count, r.server) for r in got] == \
                [(r.first_token_time, r.finish_time, r.preempt_count, r.server) for r in want], (bal, pol)
-    n_calls = len(oracle_device.calls)
-    mixed = [build_engine(EngineSettings(policy=p, pool_blocks=900)) for p in ("fcfs", "larry", "fcfs")]
-    with pytest.raises(NotImplementedError):
-        B.run_cluster(settings, trace, engines=mixed)
-    assert len(oracle_device.calls) == n_calls
+    mk = lambda: [build_engine(EngineSettings(policy=p, pool_blocks=900, c=0.5)) for p in ("fcfs", "larry", "trail_plus")]  # noqa: E731
+    want = run_cluster(settings, trace, engines=mk())
+    got = B.run_cluster(settings, trace, engines=mk())
+    assert [(r.first_token_time, r.finish_time, r.preempt_count, r.server) for r in got] == \
+           [(r.first_token_time, r.finish_time, r.preempt_count, r.server) for r in want], "mixed policies"

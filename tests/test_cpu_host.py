@@ -77,15 +77,14 @@ def test_prepare_plans_heterogeneous_servers():
     assert total >= inst[0]["scratch_offset"] + 3 * inst[0]["server_stride"]
 
 
-def test_heterogeneous_engines_need_one_policy_kind():
-    """Mixed policy kinds in one cluster are refused before any device work."""
+def test_heterogeneous_engines_at_most_120():
+    """More than 120 differing engines (beyond the pipelined cluster kernel) are refused before
+    any device work."""
     tr = P.synthesize(P.SynthSpec(duration_s=5, mean_qps=3, seed=1))
-    cs = P.ClusterSettings(2, P.EngineSettings())
-    mk = lambda pol, bs: P.Engine(P.KvBlockPool(2000, bs), P.make_policy(pol), P.default_params("llama3-8b", "a100"),  # noqa: E731
-                                  block_size=bs)
-    for a, b in ((("fcfs", 16), ("larry", 16)), (("trail_plus", 8), ("nopreempt", 8))):
-        with pytest.raises(NotImplementedError):
-            P.run_cluster(cs, tr, engines=[mk(*a), mk(*b)])
+    cs = P.ClusterSettings(121, P.EngineSettings())
+    mk = lambda pol: P.Engine(P.KvBlockPool(2000, 16), P.make_policy(pol), P.default_params("llama3-8b", "a100"))  # noqa: E731
+    with pytest.raises(NotImplementedError):
+        P.run_cluster(cs, tr, engines=[mk("fcfs")] * 60 + [mk("larry")] * 61)
 
 
 def test_synthesize_is_bit_identical_to_reference():
