@@ -101,9 +101,9 @@ typedef struct {
    * that differ, cluster.py:66-79): n_servers parameter sets, server s batching, allocating
    * and costing with its own; NULL = every server uses `engine`. h_servers is the host array
    * (read by ssb_prepare / ssb_simulate's planning), d_servers a device copy of it (read by
-   * the kernels), policy included (each engine warp runs its own server's policy). Such an
-   * instance must fit the pipelined cluster kernel (2..120 servers); otherwise ssb_simulate
-   * returns SSB_E_ARG. */
+   * the kernels), policy included (each engine warp of the pipelined kernel runs its own
+   * server's policy); beyond 120 servers (the epoch kernel, several servers per warp) the sets
+   * must share the policy, else ssb_simulate returns SSB_E_ARG. */
   const ssb_engine_params* h_servers;
   const ssb_engine_params* d_servers;
   int64_t server_stride;        /* filled by ssb_prepare(): scratch bytes per server   */

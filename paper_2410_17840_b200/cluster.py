@@ -230,10 +230,14 @@ def run_cluster(settings: ClusterSettings, trace, *, engines: list[Engine] | Non
 
 
 def check_heterogeneous(res: list) -> None:
-    """Engines of one cluster may differ in every parameter, policy included: each server runs
-    with its own set on the pipelined cluster kernel, which holds up to 120 replicas."""
-    if len(res) > 120:
-        raise NotImplementedError("heterogeneous engines: at most 120 servers (the pipelined cluster kernel)")
+    """Engines of one cluster may differ in every parameter, policy included: up to 120 replicas
+    each engine warp of the pipelined cluster kernel runs its own server's policy; beyond that
+    the epoch kernel (several servers per warp) needs one policy kind."""
+    from .policies import policy_descriptor
+
+    if len(res) > 120 and len({policy_descriptor(r.policy)[0] for r in res}) != 1:
+        raise NotImplementedError("more than 120 engines of different policies in one cluster are not supported "
+                                  "on the device")
 
 
 def event_log_with_details(ev) -> list[tuple[str, float, int, str]]:

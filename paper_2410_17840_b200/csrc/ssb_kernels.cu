@@ -534,24 +534,43 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
   // cluster (<= 8 replicas) uses the cheaper CTA barrier
   auto csync = [&]() { if (G == 1) __syncthreads(); else cl.sync(); };
   auto tab_of = [&](int s) { return tabs_in_smem ? sm_tabs + ((s / GW) * nwarps + warp) * SM_COLS * RS : nullptr; };
-  if (I.d_servers != nullptr) {  // one parameter set per warp's servers: heterogeneous engines need k_cluster_pipe
-    if (rank == 0 && threadIdx.x == 0) {
-      ssb_stats out = {};
-      out.status = SSB_E_ARG;
-      stats[idx] = out;
+  if (I.d_servers != nullptr) {  // heterogeneous engines here: one policy (a warp runs several servers)
+    bool mixed = false;
+    for (int q = 1; q < n; ++q) mixed |= I.d_servers[q].policy != I.d_servers[0].policy;
+    if (mixed) {
+      if (rank == 0 && threadIdx.x == 0) {
+        ssb_stats out = {};
+        out.status = SSB_E_ARG;
+        stats[idx] = out;
+      }
+      return;  // (every CTA of the cluster returns before its first cluster barrier)
     }
-    return;
   }
   Cfg cfg = make_cfg(I);
   cfg.policy = POL;
   const Layout L = inst_layout(I);
   ssb_event* evb = events ? events + (long long)idx * ev_cap : nullptr;
+  // server s's engine: its own parameters and tree offsets when the prebuilt engines differ
+  auto bind_server = [&](Eng& E, int s) {
+    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab_of(s));
+    if (I.d_servers != nullptr) {  // (rare: only the parameter-dependent parts are rebound)
+      const Cfg cs = make_cfg(I, server_params(I, s));
+      const Layout Ls = server_layout(I, s);
+      const int rc = E.cfg.Rc;  // (bind_engine may have clipped it to the shared table)
+      E.cfg = cs;
+      E.cfg.policy = POL;
+      E.cfg.Rc = rc;
+      unsigned char* base = scratch + I.scratch_offset + (long long)s * L.total;
+      E.p.t_head = (int*)(base + Ls.t_head);
+      E.p.t_lv = (int*)(base + Ls.t_lv);
+    }
+  };
 
   // init engines + view (cluster.py:122: refresh at 0.0 from ground truth = empty engines)
   for (int s = gw; s < n; s += GW) {
     Eng E;
-    bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab_of(s));
-    init_srv(E.st, cfg);
+    bind_server(E, s);
+    init_srv(E.st, E.cfg);
     if (cfg.policy == SSB_POLICY_TRAIL_PLUS) E.trail_init();
     fill_events(E, lane, 32);
     if (lane == 0) *(Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv) = E.st;
@@ -559,7 +578,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
   if (rank == 0) {
     for (int s = threadIdx.x; s < n; s += blockDim.x) {
       v_q[s] = 0;
-      v_f[s] = (long long)cfg.pool * cfg.bs;
+      v_f[s] = (long long)server_params(I, s).pool_blocks * server_params(I, s).block_size;
       v_if[s] = 0;
       rps[s] = 0;
       cnt[s] = 0;
@@ -695,7 +714,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
           for (int s = lane; s < n; s += 32) {
             const Srv* sv = (const Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
             v_q[s] = sv->wpend_sum + (rps[s] - sv->enq_prompt_sum);
-            v_f[s] = (long long)sv->free_blocks * cfg.bs;
+            v_f[s] = (long long)sv->free_blocks * server_params(I, s).block_size;
             v_if[s] = (long long)sv->W + sv->R + (cnt[s] - sv->next_arr);
           }
           __syncwarp();
@@ -821,7 +840,7 @@ __device__ __forceinline__ void cluster_body(const ssb_instance* __restrict__ in
     for (int s = gw; s < n; s += GW) {
       if (!(s_nb[s] < t_lim)) continue;  // no boundary before t_lim: advance would do nothing
       Eng E;
-      bind_engine(E, I, cfg, scratch, s, L, tr, rec, evb, ev_cap, tab_of(s));
+      bind_server(E, s);
       Srv* sp = (Srv*)(scratch + I.scratch_offset + (long long)s * L.total + L.srv);
       E.st = *sp;
       const long long c0 = E.st.fin_cnt, i0 = E.st.fin_in, o0 = E.st.fin_out;
@@ -1780,7 +1799,10 @@ extern "C" int32_t ssb_simulate(const ssb_instance* h_inst, const ssb_instance* 
     if (I.n_servers < 1 || I.n_requests < 0 || I.n_requests > 0x7fffffffLL || I.wait_cap < 1 || I.run_cap < 1)
       return SSB_E_ARG;
     if (I.h_servers != nullptr) {  // heterogeneous engines: one policy and block size, pipelined kernel
-      if (I.d_servers == nullptr || I.n_servers < 2 || I.n_servers > PIPE_MAX_SERVERS) return SSB_E_ARG;
+      if (I.d_servers == nullptr || I.n_servers < 2) return SSB_E_ARG;
+      if (I.n_servers > PIPE_MAX_SERVERS)  // the epoch kernel: one policy for all servers
+        for (int s = 1; s < I.n_servers; ++s)
+          if (I.h_servers[s].policy != I.h_servers[0].policy) return SSB_E_ARG;
       if (I.server_stride < inst_layout(I).total) return SSB_E_ARG;  // not prepared
     }
     const int n_sets = I.h_servers != nullptr ? I.n_servers : 1;

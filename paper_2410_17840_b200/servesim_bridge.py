@@ -268,8 +268,9 @@ def run_cluster(settings, trace, *, engines=None, record_events: bool = False):
     keys = [_engine_key(e) for e in engines]
     servers = None
     if len(set(keys)) != 1:  # prebuilt engines that differ: each server with its own parameters
-        if n > 120:
-            raise NotImplementedError("heterogeneous engines: at most 120 servers on the device")
+        if n > 120 and len({k[0] for k in keys}) != 1:
+            raise NotImplementedError("more than 120 engines of different policies in one cluster are not "
+                                      "supported on the device")
         servers = np.array([engine_params(e) for e in engines], dtype=_abi.ENGINE_PARAMS)
     arr, prm, out = _trace_columns(trace)
     _validate(engines, arr, prm, out, R)

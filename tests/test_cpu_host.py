@@ -77,9 +77,9 @@ def test_prepare_plans_heterogeneous_servers():
     assert total >= inst[0]["scratch_offset"] + 3 * inst[0]["server_stride"]
 
 
-def test_heterogeneous_engines_at_most_120():
-    """More than 120 differing engines (beyond the pipelined cluster kernel) are refused before
-    any device work."""
+def test_heterogeneous_engines_over_120_need_one_policy():
+    """More than 120 engines of different policies (beyond the pipelined cluster kernel) are
+    refused before any device work."""
     tr = P.synthesize(P.SynthSpec(duration_s=5, mean_qps=3, seed=1))
     cs = P.ClusterSettings(121, P.EngineSettings())
     mk = lambda pol: P.Engine(P.KvBlockPool(2000, 16), P.make_policy(pol), P.default_params("llama3-8b", "a100"))  # noqa: E731

@@ -227,3 +227,36 @@ def test_gpu_heterogeneous_engines_reference_binding():
         assert records_sha([r.first_token_time for r in recs], [r.finish_time for r in recs],
                            [r.preempt_count for r in recs], [r.server for r in recs]) == g["records_sha"], sc["name"]
         assert [[e.iterations, e.peak_batch_tokens] for e in engines] == [[p[0], p[3]] for p in g["per_engine"]]
+
+
+def test_gpu_heterogeneous_engines_above_pipeline_limit_match_oracle():
+    """130 prebuilt engines that differ in pool, block size, cap and costs (one policy: the epoch
+    kernel, several servers per warp, global tables) against the oracle, sal and p2c."""
+    from oracle import oracle as O
+    import paper_2410_17840_b200 as P
+    from paper_2410_17840_b200 import _abi
+    from paper_2410_17840_b200 import instances as I
+
+    trace = P.synthesize(P.SynthSpec(duration_s=30.0, mean_qps=90.0, burstiness=2.0, seed=12))
+    jobs, servers = [], {}
+    rng = np.random.default_rng(3)
+    for k, (pol, bal) in enumerate((("larry", "sal"), ("trail_plus", "p2c"))):
+        cs = P.ClusterSettings(130, P.EngineSettings(policy=pol, pool_blocks=700, c=0.5), P.BalancerSettings(bal, poll_interval_s=0.02), 5)
+        jobs.append((cs, trace, 1.0))
+    batch = I.make_batch(jobs)
+    for k in range(len(jobs)):
+        srv = np.zeros(130, dtype=_abi.ENGINE_PARAMS)
+        srv[:] = batch.instances[k]["engine"]
+        bsz = rng.choice([8, 16, 32], 130)
+        srv["block_size"] = bsz
+        srv["pool_blocks"] = (8192 // bsz + 1) + rng.integers(0, 600, 130)
+        srv["max_tokens_per_batch"] = rng.choice([256, 1024, 2048], 130)
+        srv["mem_per_kv_token_s"] = srv["mem_per_kv_token_s"] * rng.choice([0.5, 1.0, 2.0], 130)
+        servers[k] = srv
+    batch.servers = servers
+    rec, st = _sim().run_batch(batch, check=True)
+    orec, ost = O.run_batch(batch, threads=2)
+    for k in ("iterations", "request_steps", "batch_tokens", "dispatches", "preempts", "finished", "digest", "status"):
+        assert np.array_equal(st[k], ost[k]), k
+    for col in ("first_token", "finish", "preempt_count", "server"):
+        assert np.array_equal(getattr(rec, col), getattr(orec, col)), col
