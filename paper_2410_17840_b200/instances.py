@@ -97,8 +97,10 @@ def instance_record(
     record_offset: int = 0,
     qps_factor: float = 1.0,
     resolved: ResolvedEngine | None = None,
+    engine_rec: np.void | None = None,
 ) -> np.void:
-    """One ssb_instance for run_cluster(settings, trace) (cluster.py:65-104)."""
+    """One ssb_instance for run_cluster(settings, trace) (cluster.py:65-104). engine_rec: the
+    resolved engine's ssb_engine_params when the caller already has it."""
     if settings.n_servers < 1:
         raise ValueError(f"n_servers must be >= 1, got {settings.n_servers}")
     bs = settings.balancer
@@ -111,7 +113,7 @@ def instance_record(
     re = resolved or resolve_engine(settings.engine)
     qps_factor = check_qps_factor(qps_factor)
     rec = np.zeros((), dtype=_abi.INSTANCE)
-    rec["engine"] = engine_params_record(re)
+    rec["engine"] = engine_params_record(re) if engine_rec is None else engine_rec
     rec["n_servers"] = settings.n_servers
     rec["balancer"] = _abi.BALANCER_IDS[bs.name]
     rec["poll_interval_s"] = float(bs.poll_interval_s)
@@ -142,6 +144,35 @@ class Batch:
 
 
 def make_batch(jobs, *, validate: bool = True) -> Batch:
+    """jobs: iterable of (settings, trace, qps_factor[, label]) -> one Batch (see
+    _make_batch_serial for the checks). A sweep repeats few (settings, trace) pairs across many
+    factors (C4: 256 pairs x 16 factors), so the per-object work runs once per distinct pair, in
+    job order of first appearance (the serial order of every check), and the per-job columns
+    are numpy gathers; a job list with an invalid factor takes the serial path, which raises the
+    reference's error at the same job the serial loop would."""
+    jobs = jobs if isinstance(jobs, list) else list(jobs)  # (keeps every keyed object alive)
+    try:
+        fac = np.asarray([j[2] if len(j) > 2 else 1.0 for j in jobs], dtype=np.float64)
+    except (TypeError, ValueError):
+        return _make_batch_serial(jobs, validate=validate)
+    if len(jobs) == 0 or not bool(np.all((fac > 0) & np.isfinite(fac))):
+        return _make_batch_serial(jobs, validate=validate)
+    pairs = [(id(j[0]), id(j[1])) for j in jobs]
+    pos = {k: q for q, k in enumerate(dict.fromkeys(pairs))}  # distinct pairs, first-appearance order
+    if len(pos) == len(jobs):
+        return _make_batch_serial(jobs, validate=validate)
+    pidx = np.fromiter(map(pos.__getitem__, pairs), dtype=np.int64, count=len(pairs))
+    first = np.unique(pidx, return_index=True)[1]  # each pair's first job, in pair order
+    sub = _make_batch_serial([jobs[i] for i in first], validate=validate)
+    inst = sub.instances[pidx]
+    n = inst["n_requests"].astype(np.int64)
+    inst["record_offset"] = np.cumsum(n) - n
+    inst["qps_factor"] = fac
+    labels = [j[3] if len(j) > 3 else None for j in jobs]
+    return Batch(sub.trace, inst, int(n.sum()), labels)
+
+
+def _make_batch_serial(jobs, *, validate: bool = True) -> Batch:
     """jobs: iterable of (settings, trace, qps_factor[, label]). Traces that are the
     same object are stored once and shared by offset (scale_qps is fused into
     the kernel's trace read).
@@ -156,7 +187,8 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
     traces: list[Trace] = []
     trace_index: dict[int, int] = {}  # id(trace) -> [index, offset, length]
     keep_alive: list = []  # every keyed object lives until the loop ends, so no id() is reused
-    base: dict[int, list] = {}  # id(settings) -> [ResolvedEngine, template index, feasibility key]
+    base: dict[int, list] = {}  # id(settings) -> [ResolvedEngine, template index, feasibility key, params]
+    engines: dict = {}  # engine settings values -> (ResolvedEngine, feasibility key, params)
     templates: list = []
     feasible: set = set()
     c_tpl: list = []
@@ -186,10 +218,22 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
         bs = base.get(id(settings))
         if bs is None:  # build_engine first (cluster.py:74-79), the balancer after the checks (:96-104)
             keep_alive.append(settings)
-            r = resolve_engine(settings.engine)
-            lim = r.limits
-            bs = base[id(settings)] = [r, -1, (policy_descriptor(r.policy), r.block_size, r.pool_blocks,
-                                               lim.max_tokens_per_batch, lim.max_running, lim.max_context)]
+            es = settings.engine
+            try:  # equal engine settings (a sweep repeats them per seed) resolve once
+                ek = (es.policy, es.alpha, es.c, es.max_output, es.profile, es.hardware, es.block_size,
+                      es.pool_blocks, es.gpu_mem_bytes, es.max_tokens_per_batch, es.max_running,
+                      tuple(sorted(es.cost.items())))
+                hit = engines.get(ek)
+            except TypeError:  # (unhashable field values: no sharing)
+                ek, hit = None, None
+            if hit is None:
+                r = resolve_engine(es)
+                lim = r.limits
+                hit = (r, (policy_descriptor(r.policy), r.block_size, r.pool_blocks, lim.max_tokens_per_batch,
+                           lim.max_running, lim.max_context), engine_params_record(r))
+                if ek is not None:
+                    engines[ek] = hit
+            bs = base[id(settings)] = [hit[0], -1, hit[1], hit[2]]
         if validate:
             fk = (tr[0], bs[2])
             if fk not in feasible:
@@ -202,7 +246,7 @@ def make_batch(jobs, *, validate: bool = True) -> Batch:
                 feasible.add(fk)
         if bs[1] < 0:  # the balancer's checks come after feasibility (cluster.py:90-104)
             bs[1] = len(templates)
-            templates.append(instance_record(settings, 0, resolved=bs[0]))
+            templates.append(instance_record(settings, 0, resolved=bs[0], engine_rec=bs[3]))
         c_tpl.append(bs[1])
         c_n.append(tr[2])
         c_toff.append(tr[1])

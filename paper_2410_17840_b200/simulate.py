@@ -78,9 +78,24 @@ def cost_features(batch: Batch) -> np.ndarray:
     oh, mb, mkv, cpt = e["overhead_s"], e["mem_base_s"], e["mem_per_kv_token_s"], e["compute_per_token_s"]
     pre = 1.0 / np.maximum(0.05, 1.0 - lam * pm * cpt)  # prefill share of the engine's time
     R = np.ones(n_inst)
+    # R <- min(rmax, 0.5 R + 0.5 max(1, lam qm L(R) pre)), L(R) = oh + max(mb + mkv R ctx, cpt R):
+    # in place, each product and sum rounded exactly as the plain expression would
+    lq = lam * qm
+    t1, t2 = np.empty(n_inst), np.empty(n_inst)
     for _ in range(60):
-        L = oh + np.maximum(mb + mkv * R * ctx, cpt * R)
-        R = np.minimum(rmax, 0.5 * R + 0.5 * np.maximum(1.0, lam * qm * L * pre))
+        np.multiply(mkv, R, out=t1)
+        t1 *= ctx
+        t1 += mb
+        np.multiply(cpt, R, out=t2)
+        np.maximum(t1, t2, out=t1)
+        t1 += oh  # L
+        t1 *= lq
+        t1 *= pre
+        np.maximum(t1, 1.0, out=t1)
+        t1 *= 0.5
+        R *= 0.5
+        R += t1
+        np.minimum(R, rmax, out=R)
     Lmax = oh + np.maximum(mb + mkv * rmax * ctx, cpt * rmax)
     out[:, 0] = nz
     out[:, 1] = np.maximum(lam * qm * Lmax * pre / rmax, 1e-3)

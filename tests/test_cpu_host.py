@@ -154,6 +154,22 @@ def test_feasibility_from_trace_maxima_is_exact():
         assert pol.feasible_by_max(maxes, bsz, pool, lim) == (not bad.any())
 
 
+def test_make_batch_pair_path_equals_serial_path():
+    """make_batch's per-(settings, trace) pair path builds the same instances, trace and labels
+    as the job-by-job loop, and a bad factor still raises the reference's error."""
+    from paper_2410_17840_b200 import configs as Cf
+
+    jobs = Cf.c4_jobs(seeds=range(2), duration_s=60.0)
+    a, b = I.make_batch(jobs), I._make_batch_serial(jobs)
+    assert a.instances.tobytes() == b.instances.tobytes() and a.labels == b.labels and a.n_records == b.n_records
+    for f in ("arrival", "prompt", "output"):
+        assert np.array_equal(getattr(a.trace, f), getattr(b.trace, f))
+    bad = list(jobs)
+    bad[100] = (bad[100][0], bad[100][1], 0.0)
+    with pytest.raises(ValueError, match="factor must be > 0"):
+        I.make_batch(bad)
+
+
 def test_custom_python_policies_are_rejected():
     class MyPolicy(P.FcfsPolicy):
         pass
