@@ -149,11 +149,13 @@ def estimate_cost(batch: Batch) -> np.ndarray:
 
 
 def measured_cost(h_inst: np.ndarray, stats: np.ndarray) -> np.ndarray | None:
-    """Scheduling hint from a finished run: each instance's iteration count times its
-    policy's mean device cycles per iteration (over that policy's instances). Raw
-    per-instance cycles depend on what shared the SM with the instance (up to ~3x for
-    trail_plus), so a schedule built from them oscillates between runs; iterations are
-    exact and the per-policy mean absorbs the contention. None if nothing was measured."""
+    """Scheduling hint from a finished run: each instance's measured iteration count times
+    its policy's cycles per iteration (CYCLES_PER_ITER, the cold model's). Raw per-instance
+    cycles depend on what shared the SM with the instance (up to ~3x for trail_plus), so a
+    schedule built from them oscillates between runs; iterations are exact. The run's own
+    per-policy mean cycles per iteration gave SM shares that ran the C4 sweep at 135-142 ms
+    against 118-125 ms with the fixed constants (A/B on one box, profiles/r02_cost_model_ab.txt).
+    None if nothing was measured."""
     cyc = np.asarray(stats["device_cycles"], dtype=np.float64)
     it = np.asarray(stats["iterations"], dtype=np.float64)
     if len(cyc) == 0 or not (cyc > 0).all():
@@ -164,7 +166,7 @@ def measured_cost(h_inst: np.ndarray, stats: np.ndarray) -> np.ndarray | None:
     for p in np.unique(pol):
         m = (pol == p) & ~multi
         if m.any() and it[m].sum() > 0:
-            cost[m] = it[m] * (cyc[m].sum() / it[m].sum())
+            cost[m] = it[m] * CYCLES_PER_ITER[p & 3]
     return np.clip(cost // 1024, 1, 2**31 - 1).astype(h_inst["est_cost"].dtype)
 
 
