@@ -8,6 +8,7 @@ without CUDA or without libssb.so every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -139,7 +140,10 @@ def estimate_cost(batch: Batch) -> np.ndarray:
         return np.zeros(0, dtype=np.int64)
     X = cost_design(batch)
     pol = inst["engine"]["policy"].astype(np.int64) & 3
-    cyc = np.exp(np.clip(np.einsum("ij,ij->i", X, ITER_COEF[pol]), 0.0, 40.0)) * CYCLES_PER_ITER[pol]
+    cpi = CYCLES_PER_ITER
+    if os.environ.get("SSB_CPI_SCALE"):  # experiments: per-policy scale of the cycles per iteration
+        cpi = cpi * np.array([float(x) for x in os.environ["SSB_CPI_SCALE"].split(",")])
+    cyc = np.exp(np.clip(np.einsum("ij,ij->i", X, ITER_COEF[pol]), 0.0, 40.0)) * cpi[pol]
     multi = inst["n_servers"] > 1
     if multi.any():
         csum = np.concatenate([[0], np.cumsum(batch.trace.output.astype(np.int64) + 1)])
