@@ -1373,6 +1373,9 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
   }
 }
 
+#ifndef SSB_PIPE_NAP_MAX
+#define SSB_PIPE_NAP_MAX 256  // ns: the engines' watermark-poll back-off cap
+#endif
 template <int POL>
 __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst, const int* __restrict__ order,
                                           ssb_trace tr, ssb_records rec, ssb_stats* __restrict__ stats,
@@ -1481,7 +1484,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
           seen = w;  // nothing to do before this watermark
         } else {
           __nanosleep(nap);  // back off: polling warps share the issue slots with working ones
-          nap = nap < 256 ? 2 * nap : 256;
+          nap = nap < SSB_PIPE_NAP_MAX ? 2 * nap : SSB_PIPE_NAP_MAX;
         }
       }
       seen = w;
