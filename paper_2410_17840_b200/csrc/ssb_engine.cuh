@@ -30,6 +30,22 @@
 
 namespace ssb {
 
+// Debug build (-DSSB_DEBUG, tools/build_variant.sh debug -DSSB_DEBUG): bounds and accounting
+// asserts on the engine's tables, rings and pool (trap with the failing condition printed);
+// compiled out otherwise. The GPU suite runs against it with SSB_LIB=<debug lib>.
+#ifdef SSB_DEBUG
+#define SSB_ASSERT(c)                                                                    \
+  do {                                                                                   \
+    if (!(c)) {                                                                          \
+      printf("SSB_ASSERT failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define SSB_ASSERT(c) do { } while (0)
+#endif
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int ST_GONE = 0;     // finished / evicted / parked during this step (compacted away)
 constexpr int ST_PREFILL = 1;  // RequestState.PREFILLING
@@ -350,14 +366,17 @@ struct Eng {
     // 1/bs (so below 1 - frac(n/bs)) whenever n < 2^32/bs, which ssb_simulate checks for
     // every token count a request can reach (prompt + output <= max_context). Branch-free:
     // one code path for every block size (a smaller hot loop than a pow2/divide branch).
+    SSB_ASSERT(tokens >= 0 && (long long)tokens + cfg.bs - 1 < (1LL << 32) / cfg.bs);
     const unsigned n = (unsigned)(tokens + cfg.bs - 1);
     return (int)(((unsigned long long)n * cfg.bmul) >> 32);
   }
   __device__ __forceinline__ int phys(int k) const {  // ring slot of logical position k
+    SSB_ASSERT(k >= 0 && k <= cfg.Wc && st.whead >= 0 && st.whead < cfg.Wc);
     int x = st.whead + k;
     return x >= cfg.Wc ? x - cfg.Wc : x;
   }
   __device__ __forceinline__ double arrival_of(int rid) const {
+    SSB_ASSERT(rid >= 0 && rid < cfg.Wc);  // (wait_cap = the instance's request count)
     return arrival[rid];  // already scaled by qps_factor (k_scale_arrivals, workload.py:193)
   }
   __device__ __forceinline__ int wkey_for(int prompt_len, int out, int gen) const {
@@ -553,6 +572,7 @@ struct Eng {
   }
   __device__ void trail_insert(int rid_flag, int pend, int rem) {
     const int id = rid_flag & 0x7fffffff;
+    SSB_ASSERT(rem >= 0 && rem < cfg.tg.nb && id < cfg.Wc && pend >= 0);
     int prev = -1, cur = p.t_head[rem];
     while (cur >= 0 && cur < id) { prev = cur; cur = t_next(cur); }
     __syncwarp();
@@ -639,6 +659,7 @@ struct Eng {
   __device__ void preempt_entry(int j, int rid, int pr, int out, int gen, int pfd, int state, int code) {
     nodisp = false;
     lc_valid = false;
+    SSB_ASSERT(j >= 0 && j < st.R && rid >= 0 && rid < cfg.Wc && nq < cfg.Rc);
     int alloc = pr + gen;  // KV tokens held
     st.free_blocks += blocks(alloc);
     if (state == ST_DECODE) st.ndec -= 1;
@@ -1078,6 +1099,7 @@ struct Eng {
         int pend = listed ? p.l_c[j] : p.w_pend[pos];
         int pr = prompt[rid];
         int t = st.R + j;
+        SSB_ASSERT(rid >= 0 && rid < cfg.Wc && t < cfg.Rc && pend >= pr);
         p.r_rid[t] = rid;
         p.r_prompt[t] = pr;
         p.r_out[t] = output[rid];
@@ -1658,6 +1680,23 @@ struct Eng {
   }
 
   // ---- Engine.step (engine.py:193-234) ----
+#ifdef SSB_DEBUG
+  // after a step: counts within the tables, and the KV pool conserved (kvmem.py:151-154
+  // conserved(): free + every running request's blocks(prompt + generated) == total)
+  __device__ void debug_check() const {
+    if (st.status) return;
+    SSB_ASSERT(st.free_blocks >= 0 && st.free_blocks <= cfg.pool && st.R >= 0 && st.R <= cfg.Rc &&
+               st.W >= 0 && st.W <= cfg.Wc && st.next_arr >= 0);
+    if (regs_ok) return;  // (the register copy of the table is authoritative)
+    long long held = 0;
+    for (int j = lane; j < st.R; j += 32) {
+      SSB_ASSERT(p.r_st[j] == ST_PREFILL || p.r_st[j] == ST_DECODE);
+      held += blocks(p.r_prompt[j] + p.r_gen[j]);
+    }
+    held = warp_sum_ll(held);
+    SSB_ASSERT(held + st.free_blocks == cfg.pool);
+  }
+#endif
   __device__ __forceinline__ void step() {
     if (!has_work()) { st.status = SSB_E_STALL; return; }
     int nd = 0, np = 0;
@@ -1780,6 +1819,9 @@ struct Eng {
       // preempted / evicted / parked requests go back to the waiting set here, in the order
       // they were queued (policy preempts, then grow evictions): one call site for every path
       if (nq) flush_pushes();
+#ifdef SSB_DEBUG
+      debug_check();
+#endif
       if (regs_ok && nodisp && st.status == SSB_OK && cfg.bs_shift >= 0)
         fast_forward(next_t < t_lim ? next_t : t_lim);
     }
