@@ -1331,6 +1331,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
       // streamlined publish of one route (no log, no match_any): the ring slot, one release,
       // the wake hint and the watermark = the next arrival's time
       cg::cluster_group cl = cg::this_cluster();
+      SSB_ASSERT(s >= 0 && s < n);
       const int base = A.cnt[s];
       while (base + 1 - *(volatile int*)&A.taken[s] > PIPE_RING) __nanosleep(64);  // flow control
       if (lane == 0) {
@@ -1349,6 +1350,7 @@ __device__ __forceinline__ void pipe_router(const ssb_instance& I, const Cfg& cf
       k_pub = k;
       continue;
     }
+    SSB_ASSERT(s >= 0 && s < n);  // cluster.py:134-135 (the reference raises for an invalid server)
     if (lane == g.nlog) { g.slog = s; g.plog = pr; }
     g.nlog += 1;
     k += 1;
@@ -1504,6 +1506,7 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
           const int i = b + lane;
           if (i < cp) {
             const int v = ld_rc_s32(&ring[i & (PIPE_RING - 1)]);
+            SSB_ASSERT(i < N && v >= 0 && v < N);  // a published route: an arrival id of this instance
             E.p.rl[i] = v;
             dep |= v;
           }
