@@ -46,7 +46,7 @@ from servesim.workload import LengthDist, SynthSpec, TraceEntry, scale_qps, synt
 import scenarios as S  # noqa: E402
 from golden_util import EVENT_CODES, event_digest, fold_digests, records_sha, trace_sha  # noqa: E402
 
-FULL_RECORD_GROUPS = {"engine_unit", "cluster_unit"}
+FULL_RECORD_GROUPS = {"engine_unit", "cluster_unit", "hetero"}
 LEAN_GROUPS = {"c6", "c2", "c3"}  # many tiny instances: counters + digests only
 
 _orig_form_batch = Engine._form_batch

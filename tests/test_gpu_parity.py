@@ -260,3 +260,30 @@ def test_gpu_heterogeneous_engines_above_pipeline_limit_match_oracle():
         assert np.array_equal(st[k], ost[k]), k
     for col in ("first_token", "finish", "preempt_count", "server"):
         assert np.array_equal(getattr(rec, col), getattr(orec, col)), col
+
+
+def test_gpu_heterogeneous_event_lines_byte_identical():
+    """Differing prebuilt engines (mixed policies / block sizes / pools): every engine's
+    event_lines() (engine.py:267-269, seq= / count= details included) through the public
+    run_cluster(engines=...) equals the reference's, for every hetero scenario small enough to
+    carry full event logs in the golden."""
+    import paper_2410_17840_b200 as P
+    from helpers import engine_resolved, scenario_settings, scenario_trace
+
+    golden = load_golden("hetero")
+    scs = [sc for sc in S.GROUPS["hetero"]() if "event_lines" in golden[sc["name"]]]
+    assert scs
+    for sc in scs:
+        g = golden[sc["name"]]
+        cs, _ = scenario_settings(sc)
+        engines = []
+        for x in sc["engines"]:
+            re = engine_resolved(x)
+            engines.append(P.Engine(P.KvBlockPool(re.pool_blocks, re.block_size), re.policy, re.cost,
+                                    max_tokens_per_batch=re.limits.max_tokens_per_batch,
+                                    max_running=re.limits.max_running, max_context=re.limits.max_context,
+                                    record_events=True))
+        recs = P.run_cluster(cs, scenario_trace(sc), engines=engines)
+        assert [[r.first_token_time, r.finish_time, r.preempt_count, r.server] for r in recs] == g["records"], sc["name"]
+        for s, e in enumerate(engines):
+            assert e.event_lines() == g["event_lines"][s], (sc["name"], s)
