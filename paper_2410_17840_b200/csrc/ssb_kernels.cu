@@ -1520,7 +1520,13 @@ __device__ __forceinline__ void pipe_body(const ssb_instance* __restrict__ inst,
       seen_hint = cp;
       const bool sync = (w & SYNC_BIT) != 0;
       const double wt = __longlong_as_double((long long)(w & ~SYNC_BIT));
+#ifndef SSB_ABORT_EVERY_SYNC
+      // the router aborts by publishing +inf with the sync bit after setting C.abort: only
+      // that word needs the (DSMEM) abort load, not every poll sync
+      if (sync && !(wt < INF) && ld_rc_s32(&C0.abort)) {
+#else
       if (sync && ld_rc_s32(&C0.abort)) {
+#endif
         if (lane == 0) *(volatile unsigned long long*)&C.snap[warp].done = w;
         break;
       }
