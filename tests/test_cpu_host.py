@@ -87,6 +87,18 @@ def test_heterogeneous_engines_over_120_need_one_policy():
         P.run_cluster(cs, tr, engines=[mk("fcfs")] * 60 + [mk("larry")] * 61)
 
 
+def test_heterogeneous_engines_each_check_feasibility():
+    """Every prebuilt engine checks every request (cluster.py:86-92), in engine order, before any
+    device work: the second engine's small pool raises the reference's message for it."""
+    tr = [P.TraceEntry(0.0, 100, 10), P.TraceEntry(0.5, 700, 20)]
+    cs = P.ClusterSettings(2, P.EngineSettings())
+    cost = P.default_params("llama3-8b", "a100")
+    big = P.Engine(P.KvBlockPool(2000, 16), P.make_policy("fcfs"), cost)
+    small = P.Engine(P.KvBlockPool(20, 16), P.make_policy("fcfs"), cost)
+    with pytest.raises(P.InfeasibleRequestError, match="request 1: needs 45 blocks at peak, pool holds 20"):
+        P.run_cluster(cs, tr, engines=[big, small])
+
+
 def test_synthesize_is_bit_identical_to_reference():
     golden = load_golden("configs")
     for sc in S.config_scenarios():
